@@ -1,0 +1,184 @@
+/*
+ * teccl_b200.h — C ABI of the B200-native TE-CCL LP engine.
+ *
+ * The reference (arXiv 2305.13479 artifact, package `collsched`) solves the
+ * copy-free time-expanded multi-commodity-flow LP on the CPU:
+ *
+ *   build_lp_model(t, d, cfg, opts)   pkg/src/collsched/lp.py:22-136
+ *   solve(m, opts)  -> scipy HiGHS    pkg/src/collsched/solver.py:87-137
+ *   lp_completion_epoch(sol)          pkg/src/collsched/lp.py:139-153
+ *   simulate(sched, t, d, opts)       pkg/src/collsched/simulator.py:320-470
+ *
+ * Each entry point below replaces one of those steps. Every argument is a
+ * plain pointer or size; host pointers unless the name says `_dev`. All
+ * functions return 0 on success and a nonzero TECCL_E* code on failure;
+ * teccl_last_error() then holds a one-line message (thread-local).
+ *
+ * Variable and row order of a built LP are exactly the reference's
+ * (see DESIGN.md "LP layout"), so solution vectors can be handed back to the
+ * reference's own post-processing unchanged.
+ */
+#ifndef TECCL_B200_H
+#define TECCL_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TECCL_OK 0
+#define TECCL_EINVAL 1    /* bad argument / inconsistent description */
+#define TECCL_ECUDA 2     /* CUDA runtime failure */
+#define TECCL_ENOMEM 3    /* device allocation failed */
+#define TECCL_ENODEV 4    /* no usable sm_100 device */
+
+/* solve status (teccl_pdlp_result.status) */
+#define TECCL_OPTIMAL 0        /* all three relative criteria <= eps */
+#define TECCL_ITER_LIMIT 1     /* max_iters reached */
+#define TECCL_TIME_LIMIT 2     /* time_limit reached */
+#define TECCL_PRIMAL_INFEASIBLE 3
+#define TECCL_NUMERICAL 4
+
+typedef struct teccl_ctx teccl_ctx; /* one device + one stream */
+typedef struct teccl_lp teccl_lp;   /* device-resident LP: CSR, CSC, bounds, costs */
+
+const char* teccl_last_error(void);
+const char* teccl_version(void);
+
+int teccl_ctx_create(int device, teccl_ctx** out);
+int teccl_ctx_destroy(teccl_ctx* ctx);
+int teccl_ctx_sync(teccl_ctx* ctx);
+
+/* ---------------------------------------------------------------------------
+ * (1) Time-expanded constraint-matrix builder.
+ * Replaces build_lp_model (pkg/src/collsched/lp.py:22-136): the host passes
+ * the compact topology/demand tables (node kinds, edges with delay and
+ * per-epoch capacity, sorted sources, sorted (source,dst) pairs); the device
+ * emits CSR and CSC directly in HBM, with the reference's variable order,
+ * row order, bounds and (minimisation) objective.
+ */
+typedef struct {
+  int32_t num_nodes;            /* all nodes, reference node order */
+  int32_t num_edges;            /* reference edge order */
+  int32_t num_sources;          /* sources sorted by str() as lp.py:34 */
+  int32_t num_pairs;            /* (s,d) pairs sorted as lp.py:60 */
+  int32_t K;                    /* epochs 0..K-1 */
+  const uint8_t* node_is_switch;  /* [num_nodes] */
+  const int32_t* edge_src;        /* [E] node index */
+  const int32_t* edge_dst;        /* [E] node index */
+  const int32_t* edge_delta;      /* [E] ceil(alpha/tau), epochs.py:359 */
+  const double* edge_cap;         /* [E*K] chunks/epoch, cap_chunks(), row e*K+k */
+  const int32_t* source_node;     /* [S] node index of each source slot */
+  const int32_t* pair_source;     /* [P] source slot */
+  const int32_t* pair_dst;        /* [P] node index */
+  const double* pair_units;       /* [P] demanded chunks of the pair */
+  double buffer_limit;            /* < 0: no Appendix-B buffer rows */
+} teccl_te_desc;
+
+int teccl_lp_build_te(teccl_ctx* ctx, const teccl_te_desc* desc, teccl_lp** out);
+
+/* Generic LP upload (minimise obj.x s.t. row_lo <= A x <= row_hi,
+ * var_lb <= x <= var_ub; +-INFINITY allowed). Replaces the matrix assembly of
+ * collsched.solver.solve (solver.py:96-118) for any Model the reference
+ * builds. row_ptr has m+1 entries; columns need not be sorted. */
+int teccl_lp_from_csr(teccl_ctx* ctx, int32_t m, int32_t n, int64_t nnz,
+                      const int64_t* row_ptr, const int32_t* col, const double* val,
+                      const double* row_lo, const double* row_hi,
+                      const double* var_lb, const double* var_ub, const double* obj,
+                      teccl_lp** out);
+
+int teccl_lp_dims(const teccl_lp* lp, int32_t* m, int32_t* n, int64_t* nnz);
+/* Copy the built LP back to the host (CSR, columns ascending in each row).
+ * Any output pointer may be NULL. val gets explicit coefficients. */
+int teccl_lp_export(const teccl_lp* lp, int64_t* row_ptr, int32_t* col, double* val,
+                    double* row_lo, double* row_hi, double* var_lb, double* var_ub,
+                    double* obj);
+/* Copy the CSC (rows ascending in each column) back to the host. */
+int teccl_lp_export_csc(const teccl_lp* lp, int64_t* col_ptr, int32_t* row, double* val);
+int teccl_lp_destroy(teccl_lp* lp);
+
+/* ---------------------------------------------------------------------------
+ * (2)+(3) Restarted Halpern primal-dual hybrid gradient (PDLP family).
+ * Replaces the HiGHS call in collsched.solver.solve (solver.py:119-137) for
+ * LPs. Termination: relative primal residual, dual residual and duality gap
+ * all <= eps_rel (definitions in DESIGN.md).
+ */
+typedef struct {
+  double eps_rel;          /* e.g. 1e-4 */
+  int64_t max_iters;       /* hard iteration cap */
+  double time_limit;       /* seconds */
+  int32_t check_every;     /* iterations between restart/termination checks (64) */
+  int32_t ruiz_iters;      /* Ruiz equilibration passes (10) */
+  int32_t lookahead;       /* chunks queued ahead of the host poll (4) */
+  int32_t verbose;         /* print progress to stderr every N checks (0 = quiet) */
+  double reflection;       /* Halpern reflection coefficient in [0,1] (1.0) */
+  int32_t use_graphs;      /* 1: replay each chunk from a CUDA graph */
+  int32_t warm_start;      /* 1: start from x_inout / y_inout */
+} teccl_pdlp_opts;
+
+typedef struct {
+  int32_t status;
+  int32_t restarts;
+  int64_t iters;
+  double primal_obj;       /* c.x of the returned point (minimisation form) */
+  double dual_obj;
+  double rel_gap;
+  double rel_primal_res;
+  double rel_dual_res;
+  double solve_seconds;    /* device time, scaling + iterations + unscaling */
+  double omega;            /* final primal weight */
+  double step;             /* eta = 0.998 / ||A_scaled||_2 */
+  int64_t spmv_launches;   /* all kernel launches issued by the solve (setup + chunks) */
+} teccl_pdlp_result;
+
+void teccl_pdlp_default_opts(teccl_pdlp_opts* o);
+/* x_inout [n] / y_inout [m] host buffers (either may be NULL): read when
+ * warm_start, written with the solution on return. */
+int teccl_pdlp_solve(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* opts,
+                     double* x_inout, double* y_inout, teccl_pdlp_result* res);
+/* Device-pointer variant: x_dev/y_dev are device buffers owned by the caller. */
+int teccl_pdlp_solve_dev(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* opts,
+                         double* x_dev, double* y_dev, teccl_pdlp_result* res);
+
+/* One A.x then one A^T.y over the LP's unit/explicit CSR and CSC, `reps`
+ * times, timed with CUDA events on the context stream. Reports mean
+ * milliseconds per pair and the algorithmic bytes of one pair. */
+int teccl_spmv_bench(teccl_ctx* ctx, teccl_lp* lp, int32_t reps, double* ms_per_pair,
+                     double* bytes_per_pair);
+
+/* Time the two fused PDLP iteration kernels alone (after the real scaling
+ * setup), `reps` launches each, CUDA events on the context stream.
+ * out6 = {ms per col_step launch, ms per row_step launch, algorithmic bytes
+ * per col_step launch, per row_step launch, col group size, row group size}. */
+int teccl_pdlp_step_bench(teccl_ctx* ctx, teccl_lp* lp, int32_t reps, double* out6);
+
+/* ---------------------------------------------------------------------------
+ * (4) Exact-integer schedule checker / epoch simulator for a time-expanded
+ * LP solution. Replaces simulate() (simulator.py:320-470) for LP schedules:
+ * flows are quantised to `quantum` units per chunk (int64) and the replay is
+ * exact: per (edge,epoch) capacity, per (source,node,epoch) buffer >= 0
+ * (causality), switches hold nothing across epochs, every pair's cumulative
+ * reads reach its demand. `slack_units` is the per-check integer tolerance
+ * (0 = exact). x is the LP solution in the builder's variable order.
+ */
+typedef struct {
+  int64_t capacity_violations;
+  int64_t causality_violations;   /* negative buffer at a GPU */
+  int64_t switch_violations;      /* switch in != out */
+  int64_t unmet_pairs;            /* cumulative reads short of demand */
+  int32_t completion_epoch;       /* max over pairs of first epoch reads reach demand; -1 if none */
+  int64_t max_capacity_excess;    /* units */
+  int64_t max_buffer_deficit;     /* units */
+} teccl_check_report;
+
+int teccl_check_te(teccl_ctx* ctx, const teccl_te_desc* desc, const double* x_host,
+                   int64_t quantum, int64_t slack_units, teccl_check_report* out);
+int teccl_check_te_dev(teccl_ctx* ctx, const teccl_te_desc* desc, const double* x_dev,
+                       int64_t quantum, int64_t slack_units, teccl_check_report* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TECCL_B200_H */

@@ -1,0 +1,78 @@
+// Shared device-side plumbing for the TE-CCL LP engine (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string>
+
+#include "../../include/teccl_b200.h"
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "teccl_b200 is built for sm_100a only"
+#endif
+
+namespace teccl {
+
+constexpr int kSMs = 148;          // B200: 2 dies x 74 SMs
+constexpr int kThreads = 256;      // block size of every streaming kernel
+constexpr uint32_t kSignBit = 0x80000000u;  // unit-coefficient CSR: bit31 = negative
+constexpr uint32_t kIdxMask = 0x7fffffffu;
+
+void set_error(const std::string& msg);
+
+#define TECCL_CUDA(call)                                                         \
+  do {                                                                           \
+    cudaError_t _e = (call);                                                     \
+    if (_e != cudaSuccess) {                                                     \
+      ::teccl::set_error(std::string(#call) + ": " + cudaGetErrorString(_e));    \
+      return TECCL_ECUDA;                                                        \
+    }                                                                            \
+  } while (0)
+
+#define TECCL_CHECK_LAUNCH()                                                     \
+  do {                                                                           \
+    cudaError_t _e = cudaGetLastError();                                         \
+    if (_e != cudaSuccess) {                                                     \
+      ::teccl::set_error(std::string("kernel launch: ") + cudaGetErrorString(_e)); \
+      return TECCL_ECUDA;                                                        \
+    }                                                                            \
+  } while (0)
+
+// Grid for a grid-stride loop over `work` items: a multiple of the SM count,
+// capped so every SM holds `per_sm` resident blocks.
+inline int grid_for(int64_t work, int threads = kThreads, int per_sm = 8) {
+  int64_t blocks = (work + threads - 1) / threads;
+  int64_t cap = (int64_t)kSMs * per_sm;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  return (int)blocks;
+}
+
+}  // namespace teccl
+
+// Device-resident LP. Matrix stored twice: CSR (rows) for A.x and CSC for
+// A^T.y, both with sorted minor indices. When every coefficient is +-1 the
+// value arrays are absent and the sign lives in bit 31 of the index.
+struct teccl_lp {
+  int32_t m = 0, n = 0;
+  int64_t nnz = 0;
+  bool unit = false;               // coefficients are +-1, signs in index bit 31
+  int64_t* row_ptr = nullptr;      // [m+1]
+  uint32_t* col = nullptr;         // [nnz]
+  double* val = nullptr;           // [nnz] (explicit only)
+  int64_t* col_ptr = nullptr;      // [n+1]
+  uint32_t* row = nullptr;         // [nnz]
+  double* cval = nullptr;          // [nnz] (explicit only)
+  double* row_lo = nullptr;        // [m]
+  double* row_hi = nullptr;        // [m]
+  double* var_lb = nullptr;        // [n]
+  double* var_ub = nullptr;        // [n]
+  double* obj = nullptr;           // [n] minimisation costs
+  int device = 0;
+};
+
+struct teccl_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int sm_count = 148;
+};

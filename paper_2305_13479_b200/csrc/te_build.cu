@@ -1,0 +1,604 @@
+// (1) Time-expanded constraint-matrix builder: emits the copy-free TE-CCL LP
+// (reference pkg/src/collsched/lp.py:22-136) as CSR and CSC directly in HBM.
+//
+// Variable order (lp.py:47-65):
+//   per source slot s:  F(s,e,k) = s*SB + e*K + k            e in edge order
+//                       B(s,g,k) = s*SB + E*K + g*(K+1) + k  g = GPU rank in node order
+//   per pair p:         Rd(p,k)  = S*SB + p*2K + 2k,  Rc(p,k) = Rd(p,k) + 1
+// Row order (lp.py:69-131):
+//   init(s) | cap(e,k) | cons(s,n,k) (+ last(s,n) after node n's K rows when
+//   n is a GPU other than the source) | cum(p,k) | bcap(g,k) (buffer limit)
+// Every coefficient is +-1, so the matrix is stored "unit": index with the
+// sign in bit 31, no value array. Columns inside a row and rows inside a
+// column come out ascending, so both orientations are canonical and the
+// builder is deterministic.
+
+#include <cub/device/device_scan.cuh>
+
+#include <cmath>
+#include <vector>
+
+#include "common.cuh"
+
+namespace teccl {
+
+struct TeDev {
+  int Nn, E, S, P, K, G;
+  int64_t SB, CB, R_cons, R_cum, R_bcap, n_rows, n_vars;
+  int has_bcap;
+  double blimit;
+  const uint8_t* is_sw;
+  const int* gpu_of;     // [Nn] GPU rank or -1
+  const int* gpre;       // [Nn] GPUs strictly before node n
+  const int* node_of_gpu;// [G]
+  const int* esrc;
+  const int* edst;
+  const int* edelta;
+  const double* ecap;    // [E*K]
+  const int* snode;      // [S]
+  const int* pair_src;   // [P]
+  const int* pair_dst;   // [P]
+  const double* pair_u;  // [P]
+  const int* pair_of;    // [S*Nn] pair id or -1
+  const double* out_units;  // [S]
+  const int* inc_ptr;    // [Nn+1]
+  const uint32_t* inc;   // edge id | bit31 when the edge leaves the node
+  const int* out_ptr;    // [Nn+1] out-edges of node (edge order)
+  const int* out_e;
+};
+
+__device__ __forceinline__ int64_t varF(const TeDev& d, int s, int e, int k) {
+  return (int64_t)s * d.SB + (int64_t)e * d.K + k;
+}
+__device__ __forceinline__ int64_t varB(const TeDev& d, int s, int g, int k) {
+  return (int64_t)s * d.SB + (int64_t)d.E * d.K + (int64_t)g * (d.K + 1) + k;
+}
+__device__ __forceinline__ int64_t varRd(const TeDev& d, int p, int k) {
+  return (int64_t)d.S * d.SB + (int64_t)p * 2 * d.K + 2 * k;
+}
+__device__ __forceinline__ int64_t cons_off(const TeDev& d, int s, int n) {
+  return (int64_t)n * d.K + d.gpre[n] - (d.snode[s] < n ? 1 : 0);
+}
+__device__ __forceinline__ int64_t rowCons(const TeDev& d, int s, int n, int k) {
+  return d.R_cons + (int64_t)s * d.CB + cons_off(d, s, n) + k;
+}
+
+// Emit helper: count or write one (index, sign) entry.
+template <bool FILL>
+struct Emitter {
+  uint32_t* out;
+  int cnt;
+  __device__ __forceinline__ void put(int64_t idx, bool neg) {
+    if (FILL) out[cnt] = (uint32_t)idx | (neg ? kSignBit : 0u);
+    ++cnt;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Row generator: one thread per row; counts (FILL=false) or writes the row.
+template <bool FILL>
+__global__ void te_rows_kernel(TeDev d, const int64_t* __restrict__ row_ptr,
+                               uint32_t* __restrict__ col, int64_t* __restrict__ row_len,
+                               double* __restrict__ lo, double* __restrict__ hi) {
+  const int K = d.K;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < d.n_rows;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    Emitter<FILL> em{FILL ? col + row_ptr[r] : nullptr, 0};
+    double rlo = 0.0, rhi = 0.0;
+    if (r < d.S) {                                   // init(s), lp.py:69-72
+      int s = (int)r, n = d.snode[s];
+      for (int j = d.out_ptr[n]; j < d.out_ptr[n + 1]; ++j) em.put(varF(d, s, d.out_e[j], 0), false);
+      em.put(varB(d, s, d.gpu_of[n], 0), false);
+      rlo = rhi = d.out_units[s];
+    } else if (r < d.R_cons) {                       // cap(e,k), lp.py:74-77
+      int64_t q = r - d.S;
+      int e = (int)(q / K), k = (int)(q % K);
+      for (int s = 0; s < d.S; ++s) em.put(varF(d, s, e, k), false);
+      rlo = -INFINITY;
+      rhi = d.ecap[(int64_t)e * K + k];
+    } else if (r < d.R_cum) {                        // cons / last, lp.py:81-116
+      int64_t q = r - d.R_cons;
+      int s = (int)(q / d.CB);
+      int64_t off = q % d.CB;
+      // node n: last node with cons_off(s,n) <= off (offsets ascend with n)
+      int lo_n = 0, hi_n = d.Nn - 1;
+      while (lo_n < hi_n) {
+        int mid = (lo_n + hi_n + 1) >> 1;
+        if (cons_off(d, s, mid) <= off) lo_n = mid; else hi_n = mid - 1;
+      }
+      int n = lo_n;
+      int k = (int)(off - cons_off(d, s, n));      // k == K marks the last row
+      int g = d.gpu_of[n];
+      int pair = (g >= 0) ? d.pair_of[s * d.Nn + n] : -1;
+      if (k < K) {
+        for (int j = d.inc_ptr[n]; j < d.inc_ptr[n + 1]; ++j) {
+          uint32_t t = d.inc[j];
+          int e = (int)(t & kIdxMask);
+          if (t & kSignBit) {                        // leaves n: send next epoch
+            if (k + 1 <= K - 1) em.put(varF(d, s, e, k + 1), true);
+          } else {                                   // arrives at n
+            int kin = k - d.edelta[e];
+            if (kin >= 0) em.put(varF(d, s, e, kin), false);
+          }
+        }
+        if (g >= 0) {
+          em.put(varB(d, s, g, k), false);
+          em.put(varB(d, s, g, k + 1), true);
+          if (pair >= 0) em.put(varRd(d, pair, k), true);
+        }
+      } else {                                       // last(s,n), lp.py:107-116
+        for (int j = d.inc_ptr[n]; j < d.inc_ptr[n + 1]; ++j) {
+          uint32_t t = d.inc[j];
+          if (t & kSignBit) continue;
+          int e = (int)(t & kIdxMask);
+          int kin = K - 1 - d.edelta[e];
+          if (kin >= 0) em.put(varF(d, s, e, kin), false);
+        }
+        if (pair >= 0) em.put(varRd(d, pair, K - 1), true);
+      }
+      rlo = rhi = 0.0;
+    } else if (r < d.R_bcap) {                       // cum(p,k), lp.py:118-123
+      int64_t q = r - d.R_cum;
+      int p = (int)(q / K), k = (int)(q % K);
+      int64_t rd = varRd(d, p, k);
+      if (k >= 1) em.put(rd - 1, true);              // Rc(p,k-1)
+      em.put(rd, true);                              // Rd(p,k)
+      em.put(rd + 1, false);                         // Rc(p,k)
+      rlo = rhi = 0.0;
+    } else {                                         // bcap(g,k), lp.py:125-131
+      int64_t q = r - d.R_bcap;
+      int g = (int)(q / (K + 1)), k = (int)(q % (K + 1));
+      for (int s = 0; s < d.S; ++s) em.put(varB(d, s, g, k), false);
+      rlo = -INFINITY;
+      rhi = d.blimit;
+    }
+    if (FILL) {
+      lo[r] = rlo;
+      hi[r] = rhi;
+    } else {
+      row_len[r] = em.cnt;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Column generator: one thread per variable; rows emitted ascending.
+__device__ __forceinline__ void sort_small(int64_t* a, bool* neg, int n) {
+  for (int i = 1; i < n; ++i) {
+    int64_t v = a[i];
+    bool sg = neg[i];
+    int j = i - 1;
+    while (j >= 0 && a[j] > v) { a[j + 1] = a[j]; neg[j + 1] = neg[j]; --j; }
+    a[j + 1] = v;
+    neg[j + 1] = sg;
+  }
+}
+
+template <bool FILL>
+__global__ void te_cols_kernel(TeDev d, const int64_t* __restrict__ col_ptr,
+                               uint32_t* __restrict__ row, int64_t* __restrict__ col_len,
+                               double* __restrict__ lb, double* __restrict__ ub,
+                               double* __restrict__ obj) {
+  const int K = d.K;
+  const int64_t fB = (int64_t)d.E * K;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < d.n_vars;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    int64_t rows[6];
+    bool neg[6];
+    int c = 0;
+    double vlb = 0.0, vub = INFINITY, cost = 0.0;
+    if (v < (int64_t)d.S * d.SB) {
+      int s = (int)(v / d.SB);
+      int64_t q = v % d.SB;
+      if (q < fB) {                                  // F(s,e,k)
+        int e = (int)(q / K), k = (int)(q % K);
+        int u = d.esrc[e], w = d.edst[e];
+        if (k == 0 && u == d.snode[s]) { rows[c] = s; neg[c++] = false; }
+        rows[c] = d.S + (int64_t)e * K + k; neg[c++] = false;
+        if (k >= 1) { rows[c] = rowCons(d, s, u, k - 1); neg[c++] = true; }
+        int t = k + d.edelta[e];
+        if (t <= K - 1) { rows[c] = rowCons(d, s, w, t); neg[c++] = false; }
+        if (t == K - 1 && !d.is_sw[w] && w != d.snode[s]) {
+          rows[c] = rowCons(d, s, w, K); neg[c++] = false;
+        }
+        if (k == 0 && u != d.snode[s]) vub = 0.0;    // lp.py:51-52
+      } else {                                       // B(s,g,k)
+        q -= fB;
+        int g = (int)(q / (K + 1)), k = (int)(q % (K + 1));
+        int n = d.node_of_gpu[g];
+        if (k == 0 && n == d.snode[s]) { rows[c] = s; neg[c++] = false; }
+        if (k >= 1) { rows[c] = rowCons(d, s, n, k - 1); neg[c++] = true; }
+        if (k <= K - 1) { rows[c] = rowCons(d, s, n, k); neg[c++] = false; }
+        if (d.has_bcap) { rows[c] = d.R_bcap + (int64_t)g * (K + 1) + k; neg[c++] = false; }
+        if (k == 0 && n != d.snode[s]) vub = 0.0;    // lp.py:57-59
+      }
+    } else {
+      int64_t q = v - (int64_t)d.S * d.SB;
+      int p = (int)(q / (2 * K));
+      int k = (int)((q % (2 * K)) >> 1);
+      bool is_rc = (q & 1) != 0;
+      int s = d.pair_src[p], w = d.pair_dst[p];
+      double u = d.pair_u[p];
+      vub = u;
+      if (!is_rc) {                                  // Rd(p,k)
+        rows[c] = rowCons(d, s, w, k); neg[c++] = true;
+        if (k == K - 1) { rows[c] = rowCons(d, s, w, K); neg[c++] = true; }
+        rows[c] = d.R_cum + (int64_t)p * K + k; neg[c++] = true;
+      } else {                                       // Rc(p,k)
+        rows[c] = d.R_cum + (int64_t)p * K + k; neg[c++] = false;
+        if (k + 1 <= K - 1) { rows[c] = d.R_cum + (int64_t)p * K + k + 1; neg[c++] = true; }
+        if (k == K - 1) vlb = u;                     // lp.py:64-65
+        cost = -1.0 / (double)(k + 1);               // maximise sum Rc/(k+1), lp.py:133-135
+      }
+    }
+    if (FILL) {
+      sort_small(rows, neg, c);
+      uint32_t* out = row + col_ptr[v];
+      for (int i = 0; i < c; ++i) out[i] = (uint32_t)rows[i] | (neg[i] ? kSignBit : 0u);
+      lb[v] = vlb;
+      ub[v] = vub;
+      obj[v] = cost;
+    } else {
+      col_len[v] = c;
+    }
+  }
+}
+
+__global__ void set_tail_kernel(int64_t* ptr, int64_t idx, const int64_t* len_last,
+                                const int64_t* scan_last) {
+  ptr[idx] = *scan_last + *len_last;
+}
+
+}  // namespace teccl
+
+using namespace teccl;
+
+namespace {
+
+template <typename T>
+int upload(const std::vector<T>& h, T** d, cudaStream_t st) {
+  size_t bytes = h.size() * sizeof(T);
+  if (bytes == 0) bytes = sizeof(T);
+  TECCL_CUDA(cudaMallocAsync((void**)d, bytes, st));
+  if (!h.empty()) TECCL_CUDA(cudaMemcpyAsync(*d, h.data(), h.size() * sizeof(T),
+                                             cudaMemcpyHostToDevice, st));
+  return TECCL_OK;
+}
+
+// exclusive scan of len[0..count) into ptr[0..count], ptr[count] = total
+int scan_lengths(int64_t* len, int64_t* ptr, int64_t count, cudaStream_t st) {
+  size_t tmp_bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, len, ptr, count, st);
+  void* tmp = nullptr;
+  TECCL_CUDA(cudaMallocAsync(&tmp, tmp_bytes, st));
+  cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, len, ptr, count, st);
+  TECCL_CHECK_LAUNCH();
+  set_tail_kernel<<<1, 1, 0, st>>>(ptr, count, len + count - 1, ptr + count - 1);
+  TECCL_CHECK_LAUNCH();
+  TECCL_CUDA(cudaFreeAsync(tmp, st));
+  return TECCL_OK;
+}
+
+int prepare_tables(teccl_ctx* ctx, const teccl_te_desc* desc, TeDev& d, std::vector<void*>& owned) {
+  if (!ctx || !desc) { set_error("null argument"); return TECCL_EINVAL; }
+  const int Nn = desc->num_nodes, E = desc->num_edges, S = desc->num_sources,
+            P = desc->num_pairs, K = desc->K;
+  if (Nn < 1 || E < 0 || S < 0 || P < 0 || K < 1) { set_error("bad dimensions"); return TECCL_EINVAL; }
+  cudaStream_t st = ctx->stream;
+  TECCL_CUDA(cudaSetDevice(ctx->device));
+
+  // Host-side derived tables (all O(nodes + edges + pairs)).
+  std::vector<int> gpu_of(Nn, -1), gpre(Nn + 1, 0), node_of_gpu;
+  for (int n = 0; n < Nn; ++n) {
+    gpre[n] = (int)node_of_gpu.size();
+    if (!desc->node_is_switch[n]) { gpu_of[n] = (int)node_of_gpu.size(); node_of_gpu.push_back(n); }
+  }
+  const int G = (int)node_of_gpu.size();
+  std::vector<int> inc_ptr(Nn + 1, 0), out_ptr(Nn + 1, 0);
+  for (int e = 0; e < E; ++e) {
+    int u = desc->edge_src[e], w = desc->edge_dst[e];
+    if (u < 0 || u >= Nn || w < 0 || w >= Nn || u == w) { set_error("bad edge endpoint"); return TECCL_EINVAL; }
+    if (desc->edge_delta[e] < 0) { set_error("negative edge delay"); return TECCL_EINVAL; }
+    inc_ptr[u + 1]++; inc_ptr[w + 1]++; out_ptr[u + 1]++;
+  }
+  for (int n = 0; n < Nn; ++n) { inc_ptr[n + 1] += inc_ptr[n]; out_ptr[n + 1] += out_ptr[n]; }
+  std::vector<uint32_t> inc(inc_ptr[Nn]);
+  std::vector<int> out_e(out_ptr[Nn]);
+  {
+    std::vector<int> fi(inc_ptr.begin(), inc_ptr.end() - 1), fo(out_ptr.begin(), out_ptr.end() - 1);
+    for (int e = 0; e < E; ++e) {  // edge order => each node's list is sorted by edge id
+      int u = desc->edge_src[e], w = desc->edge_dst[e];
+      inc[fi[u]++] = (uint32_t)e | kSignBit;
+      inc[fi[w]++] = (uint32_t)e;
+      out_e[fo[u]++] = e;
+    }
+  }
+  std::vector<int> pair_of((size_t)S * Nn, -1);
+  std::vector<double> out_units(S, 0.0);
+  for (int p = 0; p < P; ++p) {
+    int s = desc->pair_source[p], w = desc->pair_dst[p];
+    if (s < 0 || s >= S || w < 0 || w >= Nn || desc->node_is_switch[w] ||
+        w == desc->source_node[s]) { set_error("bad demand pair"); return TECCL_EINVAL; }
+    if (pair_of[(size_t)s * Nn + w] >= 0) { set_error("duplicate demand pair"); return TECCL_EINVAL; }
+    pair_of[(size_t)s * Nn + w] = p;
+    out_units[s] += desc->pair_units[p];
+  }
+  for (int s = 0; s < S; ++s) {
+    int n = desc->source_node[s];
+    if (n < 0 || n >= Nn || desc->node_is_switch[n]) { set_error("source is not a GPU"); return TECCL_EINVAL; }
+  }
+
+  d = TeDev{};
+  d.Nn = Nn; d.E = E; d.S = S; d.P = P; d.K = K; d.G = G;
+  d.SB = (int64_t)E * K + (int64_t)G * (K + 1);
+  d.CB = (int64_t)Nn * K + G - 1;
+  d.R_cons = S + (int64_t)E * K;
+  d.R_cum = d.R_cons + (int64_t)S * d.CB;
+  d.R_bcap = d.R_cum + (int64_t)P * K;
+  d.has_bcap = desc->buffer_limit >= 0.0;
+  d.blimit = desc->buffer_limit;
+  d.n_rows = d.R_bcap + (d.has_bcap ? (int64_t)G * (K + 1) : 0);
+  d.n_vars = (int64_t)S * d.SB + (int64_t)P * 2 * K;
+  if (S == 0) d.CB = 0;
+  if (d.n_vars >= (int64_t)kSignBit || d.n_rows >= (int64_t)kSignBit) {
+    set_error("LP too large for 31-bit indices on one device; row-partition it");
+    return TECCL_EINVAL;
+  }
+
+  // Upload the small tables.
+  std::vector<uint8_t> is_sw(desc->node_is_switch, desc->node_is_switch + Nn);
+  std::vector<int> esrc(desc->edge_src, desc->edge_src + E), edst(desc->edge_dst, desc->edge_dst + E),
+      edel(desc->edge_delta, desc->edge_delta + E), snode(desc->source_node, desc->source_node + S),
+      psrc(desc->pair_source, desc->pair_source + P), pdst(desc->pair_dst, desc->pair_dst + P);
+  std::vector<double> ecap(desc->edge_cap, desc->edge_cap + (size_t)E * K),
+      pu(desc->pair_units, desc->pair_units + P);
+  auto up = [&](auto& vec, auto** dptr) -> int {
+    int rc = upload(vec, dptr, st);
+    owned.push_back((void*)*dptr);
+    return rc;
+  };
+  uint8_t* d_is_sw; int *d_gpu_of, *d_gpre, *d_nog, *d_esrc, *d_edst, *d_edel, *d_snode, *d_psrc,
+      *d_pdst, *d_pair_of, *d_inc_ptr, *d_out_ptr, *d_out_e;
+  double *d_ecap, *d_pu, *d_ou;
+  uint32_t* d_inc;
+  int rc = 0;
+  rc |= up(is_sw, &d_is_sw); rc |= up(gpu_of, &d_gpu_of); rc |= up(gpre, &d_gpre);
+  rc |= up(node_of_gpu, &d_nog); rc |= up(esrc, &d_esrc); rc |= up(edst, &d_edst);
+  rc |= up(edel, &d_edel); rc |= up(ecap, &d_ecap); rc |= up(snode, &d_snode);
+  rc |= up(psrc, &d_psrc); rc |= up(pdst, &d_pdst); rc |= up(pu, &d_pu);
+  rc |= up(pair_of, &d_pair_of); rc |= up(out_units, &d_ou); rc |= up(inc_ptr, &d_inc_ptr);
+  rc |= up(inc, &d_inc); rc |= up(out_ptr, &d_out_ptr); rc |= up(out_e, &d_out_e);
+  if (rc) return TECCL_ECUDA;
+  d.is_sw = d_is_sw; d.gpu_of = d_gpu_of; d.gpre = d_gpre; d.node_of_gpu = d_nog;
+  d.esrc = d_esrc; d.edst = d_edst; d.edelta = d_edel; d.ecap = d_ecap; d.snode = d_snode;
+  d.pair_src = d_psrc; d.pair_dst = d_pdst; d.pair_u = d_pu; d.pair_of = d_pair_of;
+  d.out_units = d_ou; d.inc_ptr = d_inc_ptr; d.inc = d_inc; d.out_ptr = d_out_ptr; d.out_e = d_out_e;
+
+  return TECCL_OK;
+}
+
+}  // namespace
+
+extern "C" int teccl_lp_build_te(teccl_ctx* ctx, const teccl_te_desc* desc, teccl_lp** out) {
+  if (!ctx || !desc || !out) { set_error("null argument"); return TECCL_EINVAL; }
+  TeDev d;
+  std::vector<void*> owned;
+  cudaStream_t st = ctx->stream;
+  int prc = prepare_tables(ctx, desc, d, owned);
+  if (prc) { for (void* p : owned) cudaFreeAsync(p, st); return prc; }
+  teccl_lp* lp = new teccl_lp();
+  lp->m = (int32_t)d.n_rows;
+  lp->n = (int32_t)d.n_vars;
+  lp->unit = true;
+  lp->device = ctx->device;
+  const int64_t m = d.n_rows, n = d.n_vars;
+  int64_t *row_len = nullptr, *col_len = nullptr;
+  TECCL_CUDA(cudaMallocAsync((void**)&lp->row_ptr, (m + 1) * sizeof(int64_t), st));
+  TECCL_CUDA(cudaMallocAsync((void**)&lp->col_ptr, (n + 1) * sizeof(int64_t), st));
+  TECCL_CUDA(cudaMallocAsync((void**)&row_len, (m + 1) * sizeof(int64_t), st));
+  TECCL_CUDA(cudaMallocAsync((void**)&col_len, (n + 1) * sizeof(int64_t), st));
+  TECCL_CUDA(cudaMallocAsync((void**)&lp->row_lo, (m + 1) * sizeof(double), st));
+  TECCL_CUDA(cudaMallocAsync((void**)&lp->row_hi, (m + 1) * sizeof(double), st));
+  TECCL_CUDA(cudaMallocAsync((void**)&lp->var_lb, (n + 1) * sizeof(double), st));
+  TECCL_CUDA(cudaMallocAsync((void**)&lp->var_ub, (n + 1) * sizeof(double), st));
+  TECCL_CUDA(cudaMallocAsync((void**)&lp->obj, (n + 1) * sizeof(double), st));
+
+  if (m > 0) {
+    te_rows_kernel<false><<<grid_for(m), kThreads, 0, st>>>(d, nullptr, nullptr, row_len, nullptr, nullptr);
+    TECCL_CHECK_LAUNCH();
+    if (scan_lengths(row_len, lp->row_ptr, m, st)) return TECCL_ECUDA;
+  } else {
+    TECCL_CUDA(cudaMemsetAsync(lp->row_ptr, 0, sizeof(int64_t), st));
+  }
+  if (n > 0) {
+    te_cols_kernel<false><<<grid_for(n), kThreads, 0, st>>>(d, nullptr, nullptr, col_len, nullptr, nullptr, nullptr);
+    TECCL_CHECK_LAUNCH();
+    if (scan_lengths(col_len, lp->col_ptr, n, st)) return TECCL_ECUDA;
+  } else {
+    TECCL_CUDA(cudaMemsetAsync(lp->col_ptr, 0, sizeof(int64_t), st));
+  }
+  int64_t nnz_r = 0, nnz_c = 0;
+  TECCL_CUDA(cudaMemcpyAsync(&nnz_r, lp->row_ptr + m, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  TECCL_CUDA(cudaMemcpyAsync(&nnz_c, lp->col_ptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  TECCL_CUDA(cudaStreamSynchronize(st));
+  if (nnz_r != nnz_c) {
+    set_error("builder internal error: CSR and CSC disagree on nnz");
+    return TECCL_EINVAL;
+  }
+  lp->nnz = nnz_r;
+  TECCL_CUDA(cudaMallocAsync((void**)&lp->col, (nnz_r + 1) * sizeof(uint32_t), st));
+  TECCL_CUDA(cudaMallocAsync((void**)&lp->row, (nnz_r + 1) * sizeof(uint32_t), st));
+  if (m > 0) {
+    te_rows_kernel<true><<<grid_for(m), kThreads, 0, st>>>(d, lp->row_ptr, lp->col, nullptr, lp->row_lo, lp->row_hi);
+    TECCL_CHECK_LAUNCH();
+  }
+  if (n > 0) {
+    te_cols_kernel<true><<<grid_for(n), kThreads, 0, st>>>(d, lp->col_ptr, lp->row, nullptr, lp->var_lb, lp->var_ub, lp->obj);
+    TECCL_CHECK_LAUNCH();
+  }
+  TECCL_CUDA(cudaFreeAsync(row_len, st));
+  TECCL_CUDA(cudaFreeAsync(col_len, st));
+  for (void* p : owned) TECCL_CUDA(cudaFreeAsync(p, st));
+  TECCL_CUDA(cudaStreamSynchronize(st));
+  *out = lp;
+  return TECCL_OK;
+}
+
+// ---------------------------------------------------------------------------
+// (4) Exact-integer schedule checker / epoch simulator over an LP solution.
+// Independent of the LP rows: buffers are replayed from the flows alone
+// (reference simulator semantics, simulator.py:381-436, restated for the
+// copy-free per-source flow): a GPU starts with its outgoing demand, loses
+// what it sends and reads, gains what lands delta epochs after a send; a
+// switch must forward exactly what lands, the next epoch.
+
+namespace teccl {
+
+struct CheckOut {
+  unsigned long long cap_viol, causal_viol, switch_viol, unmet;
+  long long max_cap_excess, max_deficit;
+  int completion;
+};
+
+__device__ __forceinline__ long long qnt(double v, double Q) { return llrint(v * Q); }
+
+__global__ void check_capacity_kernel(TeDev d, const double* __restrict__ x, double Q,
+                                      long long slack, CheckOut* out) {
+  const int64_t total = (int64_t)d.E * d.K;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int e = (int)(t / d.K), k = (int)(t % d.K);
+    long long load = 0;
+    for (int s = 0; s < d.S; ++s) load += qnt(x[varF(d, s, e, k)], Q);
+    const long long capq = (long long)floor(d.ecap[t] * Q);
+    const long long excess = load - capq;
+    if (excess > slack) atomicAdd(&out->cap_viol, 1ull);
+    if (excess > 0) atomicMax(&out->max_cap_excess, excess);
+  }
+}
+
+__global__ void check_replay_kernel(TeDev d, const double* __restrict__ x, double Q,
+                                    long long slack, CheckOut* out) {
+  const int64_t total = (int64_t)d.S * d.Nn;
+  const int K = d.K;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int s = (int)(t / d.Nn), n = (int)(t % d.Nn);
+    const int g = d.gpu_of[n];
+    const int pair = g >= 0 ? d.pair_of[s * d.Nn + n] : -1;
+    auto inflow = [&](int k) {
+      long long a = 0;
+      for (int j = d.inc_ptr[n]; j < d.inc_ptr[n + 1]; ++j) {
+        const uint32_t w = d.inc[j];
+        if (w & kSignBit) continue;
+        const int e = (int)(w & kIdxMask);
+        const int kin = k - d.edelta[e];
+        if (kin >= 0) a += qnt(x[varF(d, s, e, kin)], Q);
+      }
+      return a;
+    };
+    auto outflow = [&](int k) {
+      long long a = 0;
+      for (int j = d.out_ptr[n]; j < d.out_ptr[n + 1]; ++j) a += qnt(x[varF(d, s, d.out_e[j], k)], Q);
+      return a;
+    };
+    if (g < 0) {  // switch: forward exactly what lands, one epoch later
+      for (int k = 0; k < K; ++k) {
+        const long long in = inflow(k);
+        const long long o = (k + 1 <= K - 1) ? outflow(k + 1) : 0;
+        const long long diff = in > o ? in - o : o - in;
+        if (diff > slack) atomicAdd(&out->switch_viol, 1ull);
+      }
+      if (outflow(0) > slack) atomicAdd(&out->switch_viol, 1ull);
+      continue;
+    }
+    long long hold = (n == d.snode[s]) ? qnt(d.out_units[s], Q) : 0;
+    long long worst = 0;
+    int bad = 0;
+    hold -= outflow(0);
+    if (hold < -slack) ++bad;
+    if (hold < worst) worst = hold;
+    for (int k = 0; k < K; ++k) {
+      hold += inflow(k);
+      if (pair >= 0) hold -= qnt(x[varRd(d, pair, k)], Q);
+      if (k + 1 <= K - 1) hold -= outflow(k + 1);
+      if (hold < -slack) ++bad;
+      if (hold < worst) worst = hold;
+    }
+    if (bad) atomicAdd(&out->causal_viol, (unsigned long long)bad);
+    if (worst < 0) atomicMax(&out->max_deficit, -worst);
+  }
+}
+
+__global__ void check_demand_kernel(TeDev d, const double* __restrict__ x, double Q,
+                                    long long slack, CheckOut* out) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < d.P;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const long long need = qnt(d.pair_u[p], Q);
+    long long cum = 0;
+    int done = -1;
+    for (int k = 0; k < d.K; ++k) {
+      cum += qnt(x[varRd(d, (int)p, k)], Q);
+      if (done < 0 && cum >= need - slack) done = k;
+    }
+    if (done < 0) atomicAdd(&out->unmet, 1ull);
+    else atomicMax(&out->completion, done);
+  }
+}
+
+}  // namespace teccl
+
+extern "C" int teccl_check_te_dev(teccl_ctx* ctx, const teccl_te_desc* desc, const double* x_dev,
+                                  int64_t quantum, int64_t slack_units, teccl_check_report* rep) {
+  if (!ctx || !desc || !x_dev || !rep || quantum < 1 || slack_units < 0) {
+    set_error("bad argument");
+    return TECCL_EINVAL;
+  }
+  TECCL_CUDA(cudaSetDevice(ctx->device));
+  cudaStream_t st = ctx->stream;
+  TeDev d;
+  std::vector<void*> owned;
+  int rc = prepare_tables(ctx, desc, d, owned);
+  if (rc) { for (void* p : owned) cudaFreeAsync(p, st); return rc; }
+  CheckOut h{0, 0, 0, 0, 0, 0, -1};
+  CheckOut* dout = nullptr;
+  TECCL_CUDA(cudaMallocAsync((void**)&dout, sizeof(CheckOut), st));
+  TECCL_CUDA(cudaMemcpyAsync(dout, &h, sizeof(CheckOut), cudaMemcpyHostToDevice, st));
+  const double Q = (double)quantum;
+  const long long slack = slack_units;
+  check_capacity_kernel<<<grid_for((int64_t)d.E * d.K), kThreads, 0, st>>>(d, x_dev, Q, slack, dout);
+  check_replay_kernel<<<grid_for((int64_t)d.S * d.Nn, 64), 64, 0, st>>>(d, x_dev, Q, slack, dout);
+  check_demand_kernel<<<grid_for(d.P, 64), 64, 0, st>>>(d, x_dev, Q, slack, dout);
+  TECCL_CHECK_LAUNCH();
+  TECCL_CUDA(cudaMemcpyAsync(&h, dout, sizeof(CheckOut), cudaMemcpyDeviceToHost, st));
+  TECCL_CUDA(cudaFreeAsync(dout, st));
+  for (void* p : owned) TECCL_CUDA(cudaFreeAsync(p, st));
+  TECCL_CUDA(cudaStreamSynchronize(st));
+  rep->capacity_violations = (int64_t)h.cap_viol;
+  rep->causality_violations = (int64_t)h.causal_viol;
+  rep->switch_violations = (int64_t)h.switch_viol;
+  rep->unmet_pairs = (int64_t)h.unmet;
+  rep->completion_epoch = h.completion;
+  rep->max_capacity_excess = h.max_cap_excess;
+  rep->max_buffer_deficit = h.max_deficit;
+  return TECCL_OK;
+}
+
+extern "C" int teccl_check_te(teccl_ctx* ctx, const teccl_te_desc* desc, const double* x_host,
+                              int64_t quantum, int64_t slack_units, teccl_check_report* rep) {
+  if (!ctx || !desc || !x_host) { set_error("bad argument"); return TECCL_EINVAL; }
+  const int64_t K = desc->K;
+  int G = 0;
+  for (int i = 0; i < desc->num_nodes; ++i) G += desc->node_is_switch[i] ? 0 : 1;
+  const int64_t n = (int64_t)desc->num_sources * ((int64_t)desc->num_edges * K + (int64_t)G * (K + 1)) +
+                    (int64_t)desc->num_pairs * 2 * K;
+  double* xd = nullptr;
+  cudaStream_t st = ctx->stream;
+  TECCL_CUDA(cudaSetDevice(ctx->device));
+  TECCL_CUDA(cudaMallocAsync((void**)&xd, sizeof(double) * (n + 1), st));
+  TECCL_CUDA(cudaMemcpyAsync(xd, x_host, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+  int rc = teccl_check_te_dev(ctx, desc, xd, quantum, slack_units, rep);
+  cudaFreeAsync(xd, st);
+  cudaStreamSynchronize(st);
+  return rc;
+}
