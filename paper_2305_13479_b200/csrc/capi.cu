@@ -223,7 +223,9 @@ extern "C" int teccl_lp_destroy(teccl_lp* lp) {
   cudaSetDevice(lp->device);
   cudaDeviceSynchronize();
   void* ptrs[] = {lp->row_ptr, lp->col, lp->val, lp->col_ptr, lp->row, lp->cval,
-                  lp->row_lo, lp->row_hi, lp->var_lb, lp->var_ub, lp->obj};
+                  lp->row_lo, lp->row_hi, lp->var_lb, lp->var_ub, lp->obj,
+                  lp->srow_off, lp->srow_w, lp->srow_idx, lp->srow_val,
+                  lp->scol_off, lp->scol_w, lp->scol_idx, lp->scol_val};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete lp;

@@ -69,6 +69,17 @@ struct teccl_lp {
   double* var_ub = nullptr;        // [n]
   double* obj = nullptr;           // [n] minimisation costs
   int device = 0;
+  // SELL-32 copies used by the PDLP iteration kernels (built on first solve)
+  bool sell_ready = false;
+  int64_t* srow_off = nullptr;
+  int32_t* srow_w = nullptr;
+  uint32_t* srow_idx = nullptr;
+  double* srow_val = nullptr;
+  int64_t* scol_off = nullptr;
+  int32_t* scol_w = nullptr;
+  uint32_t* scol_idx = nullptr;
+  double* scol_val = nullptr;
+  int64_t srow_entries = 0, scol_entries = 0;
 };
 
 struct teccl_ctx {
@@ -76,3 +87,6 @@ struct teccl_ctx {
   cudaStream_t stream = nullptr;
   int sm_count = 148;
 };
+
+// Build the SELL-32 copies of lp's CSR and CSC on `st` (idempotent).
+int teccl_build_sell(teccl_lp* lp, cudaStream_t st);

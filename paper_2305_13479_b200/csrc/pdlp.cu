@@ -17,6 +17,7 @@
 // gamma = ||c_s||+1. The matrix is never rewritten: R and C are folded into
 // the gathered vectors, so the unit (+-1) TE-CCL matrix streams 4 bytes/nnz.
 
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -50,34 +51,67 @@ struct Vecs {
   double *y, *y0, *yt, *ry, *ryt;
   // unscaled data for KKT
   const double *c_u, *lb_u, *ub_u, *lo_u, *hi_u;
-  double* part;    // [kNQ * kGrid]
+  double* part;    // [kNQ * pstride]
+  int64_t pstride; // partial slots per quantity (>= every grid)
+  int nb_row, nb_col;  // blocks of the row / column tile kernels
   PdlpState* st;
 };
 
 // ---------------------------------------------------------------------------
-// Segmented group dot product: GS lanes cooperate on one row/column.
-template <int GS, bool UNIT>
-__device__ __forceinline__ double group_dot(const int64_t* __restrict__ ptr,
-                                            const uint32_t* __restrict__ idx,
-                                            const double* __restrict__ val,
-                                            const double* __restrict__ v, int64_t r, bool valid,
-                                            int glane) {
-  double s = 0.0;
-  if (valid) {
-    const int64_t b = ptr[r], e = ptr[r + 1];
-    for (int64_t p = b + glane; p < e; p += GS) {
-      const uint32_t t = __ldg(idx + p);
+// SELL-32 SpMV. The iteration matrices are re-laid out once per LP as
+// sliced ELLPACK with slice height 32 (one warp): slice s holds rows
+// 32s..32s+31, padded to the slice's longest row, stored column-major inside
+// the slice, so entry q of every row of a warp sits in one 128-byte line.
+// Padding entries point at a sentinel vector element that is always 0.
+// Index loads are perfectly coalesced, trip counts are warp-uniform, no
+// shared memory or barriers are needed, and the row order is unchanged so the
+// epilogue stays thread-per-row (padding: 2 % rows, 9 % columns on configs[1]).
+constexpr int kSlice = 32;
+constexpr int kTile = kThreads;  // rows (columns) per block of the step kernels
+
+struct SellView {
+  const int64_t* off;    // [nslices] first entry of the slice
+  const int32_t* width;  // [nslices] entries per row in the slice
+  const uint32_t* idx;   // slice-major, column-major inside a slice
+  const double* val;     // explicit coefficients (nullptr for unit LPs)
+  int64_t count;         // rows (or columns)
+};
+
+template <bool UNIT>
+__device__ __forceinline__ double sell_dot(const SellView& S, int64_t r,
+                                           const double* __restrict__ v) {
+  const int64_t s = r >> 5;
+  const int w = __ldg(S.width + s);
+  const int64_t base = __ldg(S.off + s) + (r & 31);
+  double acc = 0.0;
+  int q = 0;
+  for (; q + 4 <= w; q += 4) {
+    uint32_t t[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) t[u] = __ldg(S.idx + base + (int64_t)(q + u) * kSlice);
+    double g[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
       if (UNIT) {
-        const double xv = __ldg(v + (t & kIdxMask));
-        s += (t & kSignBit) ? -xv : xv;
+        const double xv = __ldg(v + (t[u] & kIdxMask));
+        g[u] = (t[u] & kSignBit) ? -xv : xv;
       } else {
-        s += __ldg(val + p) * __ldg(v + t);
+        g[u] = __ldg(S.val + base + (int64_t)(q + u) * kSlice) * __ldg(v + t[u]);
       }
     }
-  }
 #pragma unroll
-  for (int o = GS / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o, GS);
-  return s;
+    for (int u = 0; u < 4; ++u) acc += g[u];
+  }
+  for (; q < w; ++q) {
+    const uint32_t t = __ldg(S.idx + base + (int64_t)q * kSlice);
+    if (UNIT) {
+      const double xv = __ldg(v + (t & kIdxMask));
+      acc += (t & kSignBit) ? -xv : xv;
+    } else {
+      acc += __ldg(S.val + base + (int64_t)q * kSlice) * __ldg(v + t);
+    }
+  }
+  return acc;
 }
 
 __device__ __forceinline__ double block_sum(double v, double* sh) {
@@ -102,172 +136,138 @@ __device__ __forceinline__ double clampd(double v, double lo, double hi) {
 
 // ---------------------------------------------------------------------------
 // Primal half-step over columns (CSC), fused with A^T.y.
-template <int GS, bool UNIT, bool CHECK>
+template <bool UNIT, bool CHECK>
 __global__ void __launch_bounds__(kThreads) col_step_kernel(
-    int32_t n, const int64_t* __restrict__ col_ptr, const uint32_t* __restrict__ rows,
-    const double* __restrict__ cval, Vecs V, int j_in_chunk) {
+    int32_t n, SellView S, Vecs V, int j_in_chunk) {
   __shared__ double sh[32];
   const PdlpState* st = V.st;
   if (st->done) return;
   const double tau = st->tau, refl = st->refl;
   const double kk = (double)(st->k_inner + j_in_chunk);
   const double lam = (kk + 1.0) / (kk + 2.0);
-  const int glane = threadIdx.x & (GS - 1);
-  const int64_t groups_per_block = kThreads / GS;
-  const int64_t first = blockIdx.x * groups_per_block + threadIdx.x / GS;
-  const int64_t stride = (int64_t)gridDim.x * groups_per_block;
-  // warp-uniform trip count: iterate on the warp's first group
-  const int64_t warp_first = blockIdx.x * groups_per_block + (threadIdx.x & ~31) / GS;
+  const int64_t j = (int64_t)blockIdx.x * kTile + threadIdx.x;
+  // epilogue operands do not depend on the SpMV: issue their loads first
+  double Cj = 0.0, xj = 0.0, cj = 0.0, lbj = 0.0, ubj = 0.0, x0 = 0.0;
+  if (j < n) {
+    Cj = V.C[j]; xj = V.x[j]; cj = V.c[j]; lbj = V.lb[j]; ubj = V.ub[j]; x0 = V.x0[j];
+  }
+  const double s = (j < n) ? sell_dot<UNIT>(S, j, V.ry) : 0.0;
   double dx = 0.0, dx0 = 0.0;
-  for (int64_t base = warp_first; base < n; base += stride) {
-    const int64_t j = first + (base - warp_first);
-    const bool valid = j < n;
-    const double s = group_dot<GS, UNIT>(col_ptr, rows, cval, V.ry, j, valid, glane);
-    if (valid && glane == 0) {
-      const double Cj = V.C[j];
-      const double xj = V.x[j];
-      const double xt = clampd(xj - tau * (V.c[j] - Cj * s), V.lb[j], V.ub[j]);
-      V.cxb[j] = Cj * (2.0 * xt - xj);
-      const double x0 = V.x0[j];
-      V.x[j] = lam * ((1.0 + refl) * xt - refl * xj) + (1.0 - lam) * x0;
-      if (CHECK) {
-        V.xt[j] = xt;
-        V.cxt[j] = Cj * xt;
-        dx += (xt - xj) * (xt - xj);
-        dx0 += (xt - x0) * (xt - x0);
-      }
+  if (j < n) {
+    const double xt = clampd(xj - tau * (cj - Cj * s), lbj, ubj);
+    V.cxb[j] = Cj * (2.0 * xt - xj);
+    V.x[j] = lam * ((1.0 + refl) * xt - refl * xj) + (1.0 - lam) * x0;
+    if (CHECK) {
+      V.xt[j] = xt;
+      V.cxt[j] = Cj * xt;
+      dx = (xt - xj) * (xt - xj);
+      dx0 = (xt - x0) * (xt - x0);
     }
   }
   if (CHECK) {
     double a = block_sum(dx, sh);
-    if (threadIdx.x == 0) V.part[Q_DX * kGrid + blockIdx.x] = a;
+    if (threadIdx.x == 0) V.part[Q_DX * V.pstride + blockIdx.x] = a;
     a = block_sum(dx0, sh);
-    if (threadIdx.x == 0) V.part[Q_DX0 * kGrid + blockIdx.x] = a;
+    if (threadIdx.x == 0) V.part[Q_DX0 * V.pstride + blockIdx.x] = a;
   }
 }
 
 // Dual half-step over rows (CSR), fused with A.xbar.
-template <int GS, bool UNIT, bool CHECK>
+template <bool UNIT, bool CHECK>
 __global__ void __launch_bounds__(kThreads) row_step_kernel(
-    int32_t m, const int64_t* __restrict__ row_ptr, const uint32_t* __restrict__ cols,
-    const double* __restrict__ val, Vecs V, int j_in_chunk) {
+    int32_t m, SellView S, Vecs V, int j_in_chunk) {
   __shared__ double sh[32];
   const PdlpState* st = V.st;
   if (st->done) return;
   const double sigma = st->sigma, refl = st->refl;
   const double kk = (double)(st->k_inner + j_in_chunk);
   const double lam = (kk + 1.0) / (kk + 2.0);
-  const int glane = threadIdx.x & (GS - 1);
-  const int64_t groups_per_block = kThreads / GS;
-  const int64_t first = blockIdx.x * groups_per_block + threadIdx.x / GS;
-  const int64_t stride = (int64_t)gridDim.x * groups_per_block;
-  const int64_t warp_first = blockIdx.x * groups_per_block + (threadIdx.x & ~31) / GS;
+  const int64_t i = (int64_t)blockIdx.x * kTile + threadIdx.x;
+  double Ri = 0.0, yi = 0.0, loi = 0.0, hii = 0.0, y0 = 0.0;
+  if (i < m) {
+    Ri = V.R[i]; yi = V.y[i]; loi = V.lo[i]; hii = V.hi[i]; y0 = V.y0[i];
+  }
+  const double s = (i < m) ? sell_dot<UNIT>(S, i, V.cxb) : 0.0;
   double dy = 0.0, dy0 = 0.0;
-  for (int64_t base = warp_first; base < m; base += stride) {
-    const int64_t i = first + (base - warp_first);
-    const bool valid = i < m;
-    const double s = group_dot<GS, UNIT>(row_ptr, cols, val, V.cxb, i, valid, glane);
-    if (valid && glane == 0) {
-      const double Ri = V.R[i];
-      const double v = Ri * s;
-      const double yi = V.y[i];
-      const double yt = yi - sigma * (v - clampd(v - yi / sigma, V.lo[i], V.hi[i]));
-      const double y0 = V.y0[i];
-      const double yn = lam * ((1.0 + refl) * yt - refl * yi) + (1.0 - lam) * y0;
-      V.y[i] = yn;
-      V.ry[i] = Ri * yn;
-      if (CHECK) {
-        V.yt[i] = yt;
-        V.ryt[i] = Ri * yt;
-        dy += (yt - yi) * (yt - yi);
-        dy0 += (yt - y0) * (yt - y0);
-      }
+  if (i < m) {
+    const double v = Ri * s;
+    const double yt = yi - sigma * (v - clampd(v - yi / sigma, loi, hii));
+    const double yn = lam * ((1.0 + refl) * yt - refl * yi) + (1.0 - lam) * y0;
+    V.y[i] = yn;
+    V.ry[i] = Ri * yn;
+    if (CHECK) {
+      V.yt[i] = yt;
+      V.ryt[i] = Ri * yt;
+      dy = (yt - yi) * (yt - yi);
+      dy0 = (yt - y0) * (yt - y0);
     }
   }
   if (CHECK) {
     double a = block_sum(dy, sh);
-    if (threadIdx.x == 0) V.part[Q_DY * kGrid + blockIdx.x] = a;
+    if (threadIdx.x == 0) V.part[Q_DY * V.pstride + blockIdx.x] = a;
     a = block_sum(dy0, sh);
-    if (threadIdx.x == 0) V.part[Q_DY0 * kGrid + blockIdx.x] = a;
+    if (threadIdx.x == 0) V.part[Q_DY0 * V.pstride + blockIdx.x] = a;
   }
 }
 
 // KKT over rows at T(z): primal residual of A.x_u and the row part of the
 // dual objective.
-template <int GS, bool UNIT>
+template <bool UNIT>
 __global__ void __launch_bounds__(kThreads) kkt_row_kernel(
-    int32_t m, const int64_t* __restrict__ row_ptr, const uint32_t* __restrict__ cols,
-    const double* __restrict__ val, Vecs V) {
+    int32_t m, SellView S, Vecs V) {
   __shared__ double sh[32];
   const PdlpState* st = V.st;
   if (st->done) return;
   const double beta = st->beta, gamma = st->gamma;
-  const int glane = threadIdx.x & (GS - 1);
-  const int64_t gpb = kThreads / GS;
-  const int64_t first = blockIdx.x * gpb + threadIdx.x / GS;
-  const int64_t stride = (int64_t)gridDim.x * gpb;
-  const int64_t warp_first = blockIdx.x * gpb + (threadIdx.x & ~31) / GS;
+  const int64_t i = (int64_t)blockIdx.x * kTile + threadIdx.x;
+  const double s = (i < m) ? sell_dot<UNIT>(S, i, V.cxt) : 0.0;
   double rp = 0.0, dobj = 0.0;
-  for (int64_t base = warp_first; base < m; base += stride) {
-    const int64_t i = first + (base - warp_first);
-    const bool valid = i < m;
-    const double s = group_dot<GS, UNIT>(row_ptr, cols, val, V.cxt, i, valid, glane);
-    if (valid && glane == 0) {
-      const double ax = beta * s;
-      const double lo = V.lo_u[i], hi = V.hi_u[i];
-      const double r = ax - clampd(ax, lo, hi);
-      rp += r * r;
-      const double yu = gamma * V.ryt[i];
-      if (yu > 0.0 && isfinite(lo)) dobj += lo * yu;
-      else if (yu < 0.0 && isfinite(hi)) dobj += hi * yu;
-    }
+  if (i < m) {
+    const double ax = beta * s;
+    const double lo = V.lo_u[i], hi = V.hi_u[i];
+    const double r = ax - clampd(ax, lo, hi);
+    rp = r * r;
+    const double yu = gamma * V.ryt[i];
+    if (yu > 0.0 && isfinite(lo)) dobj = lo * yu;
+    else if (yu < 0.0 && isfinite(hi)) dobj = hi * yu;
   }
   double a = block_sum(rp, sh);
-  if (threadIdx.x == 0) V.part[Q_RP * kGrid + blockIdx.x] = a;
+  if (threadIdx.x == 0) V.part[Q_RP * V.pstride + blockIdx.x] = a;
   a = block_sum(dobj, sh);
-  if (threadIdx.x == 0) V.part[Q_DOBJ_ROW * kGrid + blockIdx.x] = a;
+  if (threadIdx.x == 0) V.part[Q_DOBJ_ROW * V.pstride + blockIdx.x] = a;
 }
 
 // KKT over columns: reduced costs, dual residual, primal objective and the
 // bound part of the dual objective.
-template <int GS, bool UNIT>
+template <bool UNIT>
 __global__ void __launch_bounds__(kThreads) kkt_col_kernel(
-    int32_t n, const int64_t* __restrict__ col_ptr, const uint32_t* __restrict__ rows,
-    const double* __restrict__ cval, Vecs V) {
+    int32_t n, SellView S, Vecs V) {
   __shared__ double sh[32];
   const PdlpState* st = V.st;
   if (st->done) return;
   const double beta = st->beta, gamma = st->gamma;
-  const int glane = threadIdx.x & (GS - 1);
-  const int64_t gpb = kThreads / GS;
-  const int64_t first = blockIdx.x * gpb + threadIdx.x / GS;
-  const int64_t stride = (int64_t)gridDim.x * gpb;
-  const int64_t warp_first = blockIdx.x * gpb + (threadIdx.x & ~31) / GS;
+  const int64_t j = (int64_t)blockIdx.x * kTile + threadIdx.x;
+  const double s = (j < n) ? sell_dot<UNIT>(S, j, V.ryt) : 0.0;
   double rd = 0.0, pobj = 0.0, dobj = 0.0;
-  for (int64_t base = warp_first; base < n; base += stride) {
-    const int64_t j = first + (base - warp_first);
-    const bool valid = j < n;
-    const double s = group_dot<GS, UNIT>(col_ptr, rows, cval, V.ryt, j, valid, glane);
-    if (valid && glane == 0) {
-      const double cj = V.c_u[j];
-      const double g = cj - gamma * s;
-      const double lb = V.lb_u[j], ub = V.ub_u[j];
-      double lamb = 0.0;
-      if (g > 0.0 && isfinite(lb)) lamb = g;
-      else if (g < 0.0 && isfinite(ub)) lamb = g;
-      const double r = g - lamb;
-      rd += r * r;
-      pobj += cj * beta * V.cxt[j];
-      if (lamb > 0.0) dobj += lamb * lb;
-      else if (lamb < 0.0) dobj += lamb * ub;
-    }
+  if (j < n) {
+    const double cj = V.c_u[j];
+    const double g = cj - gamma * s;
+    const double lb = V.lb_u[j], ub = V.ub_u[j];
+    double lamb = 0.0;
+    if (g > 0.0 && isfinite(lb)) lamb = g;
+    else if (g < 0.0 && isfinite(ub)) lamb = g;
+    const double r = g - lamb;
+    rd = r * r;
+    pobj = cj * beta * V.cxt[j];
+    if (lamb > 0.0) dobj = lamb * lb;
+    else if (lamb < 0.0) dobj = lamb * ub;
   }
   double a = block_sum(rd, sh);
-  if (threadIdx.x == 0) V.part[Q_RD * kGrid + blockIdx.x] = a;
+  if (threadIdx.x == 0) V.part[Q_RD * V.pstride + blockIdx.x] = a;
   a = block_sum(pobj, sh);
-  if (threadIdx.x == 0) V.part[Q_POBJ * kGrid + blockIdx.x] = a;
+  if (threadIdx.x == 0) V.part[Q_POBJ * V.pstride + blockIdx.x] = a;
   a = block_sum(dobj, sh);
-  if (threadIdx.x == 0) V.part[Q_DOBJ_COL * kGrid + blockIdx.x] = a;
+  if (threadIdx.x == 0) V.part[Q_DOBJ_COL * V.pstride + blockIdx.x] = a;
 }
 
 // Single block: reduce the partials in a fixed order, evaluate termination,
@@ -278,8 +278,10 @@ __global__ void __launch_bounds__(1024) control_kernel(Vecs V) {
   PdlpState* st = V.st;
   if (st->done) return;
   for (int k = 0; k < kNQ; ++k) {
+    const bool row_q = (k == Q_DY || k == Q_DY0 || k == Q_RP || k == Q_DOBJ_ROW);
+    const int nb = row_q ? V.nb_row : V.nb_col;
     double a = 0.0;
-    for (int b = threadIdx.x; b < kGrid; b += blockDim.x) a += V.part[k * kGrid + b];
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) a += V.part[k * V.pstride + b];
     a = block_sum(a, sh);
     if (threadIdx.x == 0) q[k] = a;
   }
@@ -552,56 +554,38 @@ int read_partials(double* dpart, int count, cudaStream_t st, double* out) {
   return TECCL_OK;
 }
 
-// Group sizes for rows/columns from the mean nnz per row/column.
-int pick_gs(double mean) {
-  int gs = 1;
-  while (gs < 32 && gs * 2 <= mean + 0.5) gs <<= 1;
-  return gs;
+SellView row_view(const teccl_lp* lp) {
+  return SellView{lp->srow_off, lp->srow_w, lp->srow_idx, lp->srow_val, lp->m};
 }
-
-template <bool UNIT, bool CHECK>
-void launch_col(int gs, cudaStream_t st, const teccl_lp* lp, const Vecs& V, int j) {
-  switch (gs) {
-#define L(G) case G: col_step_kernel<G, UNIT, CHECK><<<kGrid, kThreads, 0, st>>>(lp->n, lp->col_ptr, lp->row, lp->cval, V, j); break;
-    L(1) L(2) L(4) L(8) L(16) default: L(32)
-#undef L
-  }
+SellView col_view(const teccl_lp* lp) {
+  return SellView{lp->scol_off, lp->scol_w, lp->scol_idx, lp->scol_val, lp->n};
 }
 template <bool UNIT, bool CHECK>
-void launch_row(int gs, cudaStream_t st, const teccl_lp* lp, const Vecs& V, int j) {
-  switch (gs) {
-#define L(G) case G: row_step_kernel<G, UNIT, CHECK><<<kGrid, kThreads, 0, st>>>(lp->m, lp->row_ptr, lp->col, lp->val, V, j); break;
-    L(1) L(2) L(4) L(8) L(16) default: L(32)
-#undef L
-  }
+void launch_col(cudaStream_t st, const teccl_lp* lp, const Vecs& V, int j) {
+  col_step_kernel<UNIT, CHECK><<<V.nb_col, kThreads, 0, st>>>(lp->n, col_view(lp), V, j);
+}
+template <bool UNIT, bool CHECK>
+void launch_row(cudaStream_t st, const teccl_lp* lp, const Vecs& V, int j) {
+  row_step_kernel<UNIT, CHECK><<<V.nb_row, kThreads, 0, st>>>(lp->m, row_view(lp), V, j);
 }
 template <bool UNIT>
-void launch_kkt(int gsr, int gsc, cudaStream_t st, const teccl_lp* lp, const Vecs& V) {
-  switch (gsr) {
-#define L(G) case G: kkt_row_kernel<G, UNIT><<<kGrid, kThreads, 0, st>>>(lp->m, lp->row_ptr, lp->col, lp->val, V); break;
-    L(1) L(2) L(4) L(8) L(16) default: L(32)
-#undef L
-  }
-  switch (gsc) {
-#define L(G) case G: kkt_col_kernel<G, UNIT><<<kGrid, kThreads, 0, st>>>(lp->n, lp->col_ptr, lp->row, lp->cval, V); break;
-    L(1) L(2) L(4) L(8) L(16) default: L(32)
-#undef L
-  }
+void launch_kkt(cudaStream_t st, const teccl_lp* lp, const Vecs& V) {
+  kkt_row_kernel<UNIT><<<V.nb_row, kThreads, 0, st>>>(lp->m, row_view(lp), V);
+  kkt_col_kernel<UNIT><<<V.nb_col, kThreads, 0, st>>>(lp->n, col_view(lp), V);
 }
 
 template <bool UNIT>
-void enqueue_chunk(int chunk, int gsr, int gsc, cudaStream_t st, const teccl_lp* lp,
-                   const Vecs& V) {
+void enqueue_chunk(int chunk, cudaStream_t st, const teccl_lp* lp, const Vecs& V) {
   for (int j = 0; j < chunk; ++j) {
     if (j == chunk - 1) {
-      launch_col<UNIT, true>(gsc, st, lp, V, j);
-      launch_row<UNIT, true>(gsr, st, lp, V, j);
+      launch_col<UNIT, true>(st, lp, V, j);
+      launch_row<UNIT, true>(st, lp, V, j);
     } else {
-      launch_col<UNIT, false>(gsc, st, lp, V, j);
-      launch_row<UNIT, false>(gsr, st, lp, V, j);
+      launch_col<UNIT, false>(st, lp, V, j);
+      launch_row<UNIT, false>(st, lp, V, j);
     }
   }
-  launch_kkt<UNIT>(gsr, gsc, st, lp, V);
+  launch_kkt<UNIT>(st, lp, V);
   control_kernel<<<1, 1024, 0, st>>>(V);
   restart_x_kernel<<<grid_for(lp->n), kThreads, 0, st>>>(lp->n, V);
   restart_y_kernel<<<grid_for(lp->m), kThreads, 0, st>>>(lp->m, V);
@@ -630,11 +614,15 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
          *cstat = W.alloc<double>(n);
   double *cs = W.alloc<double>(n), *lbs = W.alloc<double>(n), *ubs = W.alloc<double>(n);
   double *los = W.alloc<double>(m), *his = W.alloc<double>(m);
+  // gathered vectors (cxb, cxt, ry, ryt) carry one extra always-zero slot:
+  // the SELL padding entries point at it
   double *x = W.alloc<double>(n), *x0 = W.alloc<double>(n), *xt = W.alloc<double>(n),
-         *cxb = W.alloc<double>(n), *cxt = W.alloc<double>(n);
+         *cxb = W.alloc<double>(n + 1), *cxt = W.alloc<double>(n + 1);
   double *y = W.alloc<double>(m), *y0 = W.alloc<double>(m), *yt = W.alloc<double>(m),
-         *ry = W.alloc<double>(m), *ryt = W.alloc<double>(m);
-  double* part = W.alloc<double>((int64_t)kNQ * kGrid);
+         *ry = W.alloc<double>(m + 1), *ryt = W.alloc<double>(m + 1);
+  const int nb_row = (int)((m + kTile - 1) / kTile), nb_col = (int)((n + kTile - 1) / kTile);
+  const int64_t pstride = std::max<int64_t>(std::max(nb_row, nb_col), kGrid);
+  double* part = W.alloc<double>((int64_t)kNQ * pstride);
   double* part2 = W.alloc<double>(kGrid);
   PdlpState* dst = W.alloc<PdlpState>(1);
   if (!R || !C || !rstat || !cstat || !cs || !lbs || !ubs || !los || !his || !x || !x0 || !xt ||
@@ -642,7 +630,15 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
     set_error("device allocation failed for PDLP workspace");
     return TECCL_ENOMEM;
   }
-  TECCL_CUDA(cudaMemsetAsync(part, 0, sizeof(double) * kNQ * kGrid, st));
+  TECCL_CUDA(cudaMemsetAsync(part, 0, sizeof(double) * kNQ * pstride, st));
+  TECCL_CUDA(cudaMemsetAsync(cxb, 0, sizeof(double) * (n + 1), st));
+  TECCL_CUDA(cudaMemsetAsync(cxt, 0, sizeof(double) * (n + 1), st));
+  TECCL_CUDA(cudaMemsetAsync(ry, 0, sizeof(double) * (m + 1), st));
+  TECCL_CUDA(cudaMemsetAsync(ryt, 0, sizeof(double) * (m + 1), st));
+  {
+    int rc = teccl_build_sell(lp, st);
+    if (rc) return rc;
+  }
   const int gr = grid_for(m > n ? m : n);
 
   // --- Ruiz equilibration + Pock-Chambolle (alpha = 1), simultaneous updates.
@@ -726,12 +722,14 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
   V.y = y; V.y0 = y0; V.yt = yt; V.ry = ry; V.ryt = ryt;
   V.c_u = lp->obj; V.lb_u = lp->var_lb; V.ub_u = lp->var_ub; V.lo_u = lp->row_lo; V.hi_u = lp->row_hi;
   V.part = part;
+  V.pstride = pstride;
+  V.nb_row = nb_row;
+  V.nb_col = nb_col;
   V.st = dst;
   init_iterates_kernel<<<gr, kThreads, 0, st>>>(n, m, V, o->warm_start, x_dev, y_dev);
   TECCL_CHECK_LAUNCH();
 
-  const int gsr = pick_gs(m > 0 ? (double)lp->nnz / m : 1.0);
-  const int gsc = pick_gs(n > 0 ? (double)lp->nnz / n : 1.0);
+  const int gsr = kTile, gsc = kTile;
 
   if (sb) {  // time the fused iteration kernels alone, CUDA events on this stream
     cudaEvent_t a, b, c2;
@@ -739,13 +737,13 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
     TECCL_CUDA(cudaEventCreate(&b));
     TECCL_CUDA(cudaEventCreate(&c2));
     for (int w = 0; w < 3; ++w) {
-      launch_col<UNIT, false>(gsc, st, lp, V, 0);
-      launch_row<UNIT, false>(gsr, st, lp, V, 0);
+      launch_col<UNIT, false>(st, lp, V, 0);
+      launch_row<UNIT, false>(st, lp, V, 0);
     }
     TECCL_CUDA(cudaEventRecord(a, st));
-    for (int r = 0; r < sb->reps; ++r) launch_col<UNIT, false>(gsc, st, lp, V, 0);
+    for (int r = 0; r < sb->reps; ++r) launch_col<UNIT, false>(st, lp, V, 0);
     TECCL_CUDA(cudaEventRecord(b, st));
-    for (int r = 0; r < sb->reps; ++r) launch_row<UNIT, false>(gsr, st, lp, V, 0);
+    for (int r = 0; r < sb->reps; ++r) launch_row<UNIT, false>(st, lp, V, 0);
     TECCL_CUDA(cudaEventRecord(c2, st));
     TECCL_CHECK_LAUNCH();
     TECCL_CUDA(cudaEventSynchronize(c2));
@@ -758,8 +756,11 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
     // algorithmic bytes: index stream once, pointer
     // array once, gathered vector once, 6 dense reads + 2 writes per column,
     // 5 dense reads + 2 writes per row
-    sb->bytes_col = 8.0 * (n + 1) + ib * lp->nnz + 8.0 * m + 64.0 * n;
-    sb->bytes_row = 8.0 * (m + 1) + ib * lp->nnz + 8.0 * n + 56.0 * m;
+    // SELL-32: slice offsets + widths (12 B per 32 rows), every stored entry
+    // (padding included) once, gathered vector once, dense operands
+    const double ns_c = (n + 31) / 32, ns_r = (m + 31) / 32;
+    sb->bytes_col = 12.0 * ns_c + ib * lp->scol_entries + 8.0 * m + 64.0 * n;
+    sb->bytes_row = 12.0 * ns_r + ib * lp->srow_entries + 8.0 * n + 56.0 * m;
     sb->gs_col = gsc;
     sb->gs_row = gsr;
     cudaEventDestroy(a); cudaEventDestroy(b); cudaEventDestroy(c2);
@@ -773,7 +774,7 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
     cudaStream_t cap;
     TECCL_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
     TECCL_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
-    enqueue_chunk<UNIT>(chunk, gsr, gsc, cap, lp, V);
+    enqueue_chunk<UNIT>(chunk, cap, lp, V);
     TECCL_CUDA(cudaStreamEndCapture(cap, &g));
     TECCL_CUDA(cudaGraphInstantiate(&gexec, g, 0));
     TECCL_CUDA(cudaGraphDestroy(g));
@@ -797,7 +798,7 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
       if (gexec) {
         TECCL_CUDA(cudaGraphLaunch(gexec, st));
       } else {
-        enqueue_chunk<UNIT>(chunk, gsr, gsc, st, lp, V);
+        enqueue_chunk<UNIT>(chunk, st, lp, V);
       }
       TECCL_CHECK_LAUNCH();
       const int slot = (int)(launched % look);
