@@ -47,7 +47,9 @@ class PdlpOpts(C.Structure):
         ("eps_rel", C.c_double), ("max_iters", C.c_int64), ("time_limit", C.c_double),
         ("check_every", C.c_int32), ("ruiz_iters", C.c_int32), ("lookahead", C.c_int32),
         ("verbose", C.c_int32), ("reflection", C.c_double), ("use_graphs", C.c_int32),
-        ("warm_start", C.c_int32),
+        ("warm_start", C.c_int32), ("restart_sufficient", C.c_double),
+        ("restart_necessary", C.c_double), ("restart_artificial", C.c_double),
+        ("omega_theta", C.c_double),
     ]
 
 

@@ -4,7 +4,10 @@
 // kernels serve the reference's own model objects.
 
 #include <algorithm>
+#include <array>
 #include <cmath>
+#include <cstring>
+#include <unordered_map>
 #include <string>
 #include <vector>
 
@@ -156,6 +159,55 @@ extern "C" int teccl_lp_from_csr(teccl_ctx* ctx, int32_t m, int32_t n, int64_t n
   rc |= to_dev(std::vector<double>(var_ub, var_ub + n), &lp->var_ub, st);
   rc |= to_dev(std::vector<double>(obj, obj + n), &lp->obj, st);
   if (rc) { set_error("device upload failed"); return TECCL_ECUDA; }
+  // bound-class dictionaries for the PDLP kernels (first-seen order)
+  {
+    struct KeyHash {
+      size_t operator()(const std::array<uint64_t, 3>& k) const {
+        uint64_t h = 1469598103934665603ull;
+        for (uint64_t v : k) { h ^= v; h *= 1099511628211ull; h ^= h >> 29; }
+        return (size_t)h;
+      }
+    };
+    auto bits = [](double v) {
+      v += 0.0;  // -0.0 -> +0.0
+      uint64_t b;
+      memcpy(&b, &v, sizeof b);
+      return b;
+    };
+    std::unordered_map<std::array<uint64_t, 3>, int, KeyHash> cmap, rmap;
+    std::vector<uint16_t> ccode(n), rcode(m);
+    std::vector<double> cdict, rdict;
+    bool cok = true, rok = true;
+    for (int32_t j = 0; j < n && cok; ++j) {
+      std::array<uint64_t, 3> k{bits(var_lb[j]), bits(var_ub[j]), bits(obj[j])};
+      auto it = cmap.find(k);
+      if (it == cmap.end()) {
+        if ((int)cmap.size() >= kMaxDict) { cok = false; break; }
+        it = cmap.emplace(k, (int)cmap.size()).first;
+        cdict.push_back(var_lb[j] + 0.0); cdict.push_back(var_ub[j] + 0.0); cdict.push_back(obj[j] + 0.0);
+      }
+      ccode[j] = (uint16_t)it->second;
+    }
+    for (int32_t i = 0; i < m && rok; ++i) {
+      std::array<uint64_t, 3> k{bits(row_lo[i]), bits(row_hi[i]), 0};
+      auto it = rmap.find(k);
+      if (it == rmap.end()) {
+        if ((int)rmap.size() >= kMaxDict) { rok = false; break; }
+        it = rmap.emplace(k, (int)rmap.size()).first;
+        rdict.push_back(row_lo[i] + 0.0); rdict.push_back(row_hi[i] + 0.0);
+      }
+      rcode[i] = (uint16_t)it->second;
+    }
+    if (cok && rok) {
+      rc |= to_dev(ccode, &lp->col_code, st);
+      rc |= to_dev(rcode, &lp->row_code, st);
+      rc |= to_dev(cdict, &lp->col_dict, st);
+      rc |= to_dev(rdict, &lp->row_dict, st);
+      lp->n_col_dict = (int32_t)cmap.size();
+      lp->n_row_dict = (int32_t)rmap.size();
+      if (rc) { set_error("device upload failed"); return TECCL_ECUDA; }
+    }
+  }
   TECCL_CUDA(cudaStreamSynchronize(st));
   *out = lp;
   return TECCL_OK;
@@ -225,7 +277,8 @@ extern "C" int teccl_lp_destroy(teccl_lp* lp) {
   void* ptrs[] = {lp->row_ptr, lp->col, lp->val, lp->col_ptr, lp->row, lp->cval,
                   lp->row_lo, lp->row_hi, lp->var_lb, lp->var_ub, lp->obj,
                   lp->srow_off, lp->srow_w, lp->srow_idx, lp->srow_val,
-                  lp->scol_off, lp->scol_w, lp->scol_idx, lp->scol_val};
+                  lp->scol_off, lp->scol_w, lp->scol_idx, lp->scol_val,
+                  lp->col_code, lp->row_code, lp->col_dict, lp->row_dict};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete lp;

@@ -80,7 +80,16 @@ struct teccl_lp {
   uint32_t* scol_idx = nullptr;
   double* scol_val = nullptr;
   int64_t srow_entries = 0, scol_entries = 0;
+  // bound classes: uint16 code per column/row into (lb,ub,c) / (lo,hi)
+  // dictionaries; nullptr when the LP has too many distinct classes
+  uint16_t* col_code = nullptr;
+  uint16_t* row_code = nullptr;
+  double* col_dict = nullptr;      // [3 * n_col_dict]
+  double* row_dict = nullptr;      // [2 * n_row_dict]
+  int32_t n_col_dict = 0, n_row_dict = 0;
 };
+
+constexpr int kMaxDict = 65536;
 
 struct teccl_ctx {
   int device = 0;

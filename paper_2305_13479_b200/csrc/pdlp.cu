@@ -1,21 +1,33 @@
 // (2)+(3) Restarted reflected-Halpern PDHG (PDLP family) on sm_100a.
 //
 // Replaces the CPU LP solve of the reference (pkg/src/collsched/solver.py:
-// 119-137, scipy.optimize.milp -> HiGHS) for the TE-CCL LP. One iteration is
-// two fused kernels:
-//   col_step: A^T.y SpMV over the CSC + primal step, projection onto bounds,
-//             reflection and Halpern averaging, emits C.(2x'-x) for the gather
-//   row_step: A.xbar SpMV over the CSR + dual step, projection onto the row
-//             bounds, Halpern averaging, emits R.y for the next gather
-// Every `check_every` iterations the chunk ends with KKT kernels (unscaled
-// residuals, objectives) and a single-block control kernel that decides
-// termination, restarts and the primal weight on the device, so the host
-// never sits in the iteration loop. Chunks are replayed from a CUDA graph.
+// 119-137, scipy.optimize.milp -> HiGHS) for the TE-CCL LP.
 //
-// Scaled problem: x = beta * C.xs, y = gamma * R.ys with
-// R, C from Ruiz + Pock-Chambolle equilibration, beta = ||b_s||+1,
-// gamma = ||c_s||+1. The matrix is never rewritten: R and C are folded into
-// the gathered vectors, so the unit (+-1) TE-CCL matrix streams 4 bytes/nnz.
+// Formulation. The iteration runs in the ORIGINAL variables with diagonal
+// preconditioners T = tau * D and S = sigma * E, where D = C^2 and E = R^2 come
+// from Ruiz + Pock-Chambolle equilibration (C, R column/row scales) and are
+// rounded to fp32 once -- the rounded values *are* the preconditioner, so the
+// rounding is exact, and the step-size bound uses the same rounded values:
+//
+//   x+ = clamp(x - tau D (c - A^T y), lb, ub)          xbar = 2 x+ - x
+//   y+ = y - sigma E (A xbar - clamp(A xbar - y/(sigma E), lo, hi))
+//   z <- lam ((1+rho) z+ - rho z) + (1-lam) z0,        lam = (k+1)/(k+2)
+//
+// This is exactly PDHG on the equilibrated problem (x = C xs, y = R ys) but
+// the matrix is never scaled, so the +-1 TE-CCL matrix streams 4 B/nnz and
+// x, y are already the unscaled solution. Bounds and costs are read through
+// per-row/per-column uint16 class codes into small dictionaries (a handful of
+// distinct (lb,ub,c) / (lo,hi) classes for the TE-CCL LP) when the LP has
+// them, else from the full fp64 arrays. Halpern anchors are fp32 (any anchor
+// is valid; it only selects which optimal point the iteration heads for).
+//
+// One iteration = two fused kernels over SELL-32 matrices (sell.cu):
+//   col_step: A^T.y + primal step + projection + reflection + Halpern, emits xbar
+//   row_step: A.xbar + dual step + projection + Halpern, emits y
+// Every `check_every` iterations the chunk ends with KKT kernels (residuals,
+// objectives at T(z)), a one-block control kernel (termination, restart,
+// primal weight -- all PDLP control flow stays on the device) and restart
+// kernels. Chunks are replayed from a CUDA graph, queued ahead of the host.
 
 #include <algorithm>
 #include <chrono>
@@ -27,88 +39,88 @@
 
 namespace teccl {
 
-constexpr int kGrid = kSMs * 8;  // blocks of every reduction-bearing kernel
+constexpr int kGrid = kSMs * 8;  // blocks of the setup reduction kernels
 constexpr int kNQ = 9;           // partial quantities per check
+constexpr int kSlice = 32;
+constexpr int kTile = kThreads;  // rows (columns) per block of the step kernels
 
 enum Q { Q_DX = 0, Q_DX0, Q_DY, Q_DY0, Q_RP, Q_DOBJ_ROW, Q_RD, Q_POBJ, Q_DOBJ_COL };
 
 struct PdlpState {
   double tau, sigma, omega, eta, refl;
-  double beta, gamma;        // bound / objective rescaling
   double bnorm, cnorm;       // unscaled norms for the relative criteria
   double eps;
   double r0, rprev, last_r;
+  double rs_suff, rs_nec, rs_art, theta;
   long long k_inner, total;
   int have_r0, restart, done, restarts, chunk_len, pad;
   double rel_p, rel_d, gap, pobj, dobj;
 };
 
+// Per-column / per-row problem data as the iteration kernels see it.
+struct Bounds {
+  const uint16_t* code;  // class code, or nullptr: read the explicit arrays
+  const double* dict;    // classes: (lb, ub, c) for columns, (lo, hi) for rows
+  const double* a;       // explicit lb (cols) / lo (rows)
+  const double* b;       // explicit ub / hi
+  const double* c;       // explicit cost (cols only)
+};
+
 struct Vecs {
-  // problem (scaled)
-  const double *c, *lb, *ub, *lo, *hi, *R, *C;
-  // iterates
-  double *x, *x0, *xt, *cxb, *cxt;
-  double *y, *y0, *yt, *ry, *ryt;
-  // unscaled data for KKT
+  const float* D;        // column preconditioner C^2
+  const float* E;        // row preconditioner R^2
+  Bounds col, row;
+  double *x, *xt, *xbar; // xbar has an always-zero slot [n] (SELL padding)
+  float* x0;
+  double *y, *yt;        // y, yt have an always-zero slot [m]
+  float* y0;
+  // exact unscaled data for the KKT evaluation
   const double *c_u, *lb_u, *ub_u, *lo_u, *hi_u;
-  double* part;    // [kNQ * pstride]
-  int64_t pstride; // partial slots per quantity (>= every grid)
-  int nb_row, nb_col;  // blocks of the row / column tile kernels
+  double* part;          // [kNQ * pstride]
+  int64_t pstride;
+  int nb_row, nb_col;
   PdlpState* st;
 };
 
 // ---------------------------------------------------------------------------
-// SELL-32 SpMV. The iteration matrices are re-laid out once per LP as
-// sliced ELLPACK with slice height 32 (one warp): slice s holds rows
-// 32s..32s+31, padded to the slice's longest row, stored column-major inside
-// the slice, so entry q of every row of a warp sits in one 128-byte line.
-// Padding entries point at a sentinel vector element that is always 0.
-// Index loads are perfectly coalesced, trip counts are warp-uniform, no
-// shared memory or barriers are needed, and the row order is unchanged so the
-// epilogue stays thread-per-row (padding: 2 % rows, 9 % columns on configs[1]).
-constexpr int kSlice = 32;
-constexpr int kTile = kThreads;  // rows (columns) per block of the step kernels
-
+// SELL-32 SpMV (layout built by sell.cu): slice s holds rows 32s..32s+31,
+// padded to the slice's longest row, column-major inside the slice, so entry
+// q of every row of a warp sits in one 128-byte line; padding points at an
+// always-zero vector slot. Coalesced index streams, warp-uniform trip counts,
+// no shared memory, no barriers; row order unchanged, so the epilogue is
+// thread-per-row with coalesced vector traffic.
 struct SellView {
-  const int64_t* off;    // [nslices] first entry of the slice
-  const int32_t* width;  // [nslices] entries per row in the slice
-  const uint32_t* idx;   // slice-major, column-major inside a slice
+  const int64_t* off;
+  const int32_t* width;
+  const uint32_t* idx;
   const double* val;     // explicit coefficients (nullptr for unit LPs)
-  int64_t count;         // rows (or columns)
+  int64_t count;
 };
 
-template <bool UNIT>
+template <bool UNIT, int G = 4>
 __device__ __forceinline__ double sell_dot(const SellView& S, int64_t r,
                                            const double* __restrict__ v) {
   const int64_t s = r >> 5;
   const int w = __ldg(S.width + s);
-  const int64_t base = __ldg(S.off + s) + (r & 31);
+  const uint32_t* ip = S.idx + __ldg(S.off + s) + (r & 31);
+  const double* vp = UNIT ? nullptr : S.val + (ip - S.idx);
   double acc = 0.0;
-  int q = 0;
-  for (; q + 4 <= w; q += 4) {
-    uint32_t t[4];
+  // groups of G entries, predicated: all index loads of a group are in
+  // flight together, then all gathers (2 latencies per group, not per entry)
+  for (int q = 0; q < w; q += G) {
+    uint32_t t[G];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) t[u] = __ldg(S.idx + base + (int64_t)(q + u) * kSlice);
-    double g[4];
+    for (int u = 0; u < G; ++u) t[u] = (q + u < w) ? __ldg(ip + (q + u) * kSlice) : 0u;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      if (UNIT) {
-        const double xv = __ldg(v + (t[u] & kIdxMask));
-        g[u] = (t[u] & kSignBit) ? -xv : xv;
-      } else {
-        g[u] = __ldg(S.val + base + (int64_t)(q + u) * kSlice) * __ldg(v + t[u]);
+    for (int u = 0; u < G; ++u) {
+      if (q + u < w) {
+        if (UNIT) {
+          const double xv = __ldg(v + (t[u] & kIdxMask));
+          acc += (t[u] & kSignBit) ? -xv : xv;
+        } else {
+          acc += __ldg(vp + (q + u) * kSlice) * __ldg(v + t[u]);
+        }
       }
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) acc += g[u];
-  }
-  for (; q < w; ++q) {
-    const uint32_t t = __ldg(S.idx + base + (int64_t)q * kSlice);
-    if (UNIT) {
-      const double xv = __ldg(v + (t & kIdxMask));
-      acc += (t & kSignBit) ? -xv : xv;
-    } else {
-      acc += __ldg(S.val + base + (int64_t)q * kSlice) * __ldg(v + t);
     }
   }
   return acc;
@@ -134,11 +146,38 @@ __device__ __forceinline__ double clampd(double v, double lo, double hi) {
   return fmin(fmax(v, lo), hi);
 }
 
+template <bool DICT>
+__device__ __forceinline__ void col_data(const Bounds& B, int64_t j, double& lb, double& ub,
+                                         double& c) {
+  if (DICT) {
+    const double* e = B.dict + 3 * (int64_t)__ldg(B.code + j);
+    lb = __ldg(e);
+    ub = __ldg(e + 1);
+    c = __ldg(e + 2);
+  } else {
+    lb = __ldg(B.a + j);
+    ub = __ldg(B.b + j);
+    c = __ldg(B.c + j);
+  }
+}
+
+template <bool DICT>
+__device__ __forceinline__ void row_data(const Bounds& B, int64_t i, double& lo, double& hi) {
+  if (DICT) {
+    const double* e = B.dict + 2 * (int64_t)__ldg(B.code + i);
+    lo = __ldg(e);
+    hi = __ldg(e + 1);
+  } else {
+    lo = __ldg(B.a + i);
+    hi = __ldg(B.b + i);
+  }
+}
+
 // ---------------------------------------------------------------------------
-// Primal half-step over columns (CSC), fused with A^T.y.
-template <bool UNIT, bool CHECK>
-__global__ void __launch_bounds__(kThreads) col_step_kernel(
-    int32_t n, SellView S, Vecs V, int j_in_chunk) {
+// Primal half-step over columns (CSC as SELL), fused with A^T.y.
+template <bool UNIT, bool DICT, bool CHECK>
+__global__ void __launch_bounds__(kThreads) col_step_kernel(int32_t n, SellView S, Vecs V,
+                                                            int j_in_chunk) {
   __shared__ double sh[32];
   const PdlpState* st = V.st;
   if (st->done) return;
@@ -146,22 +185,25 @@ __global__ void __launch_bounds__(kThreads) col_step_kernel(
   const double kk = (double)(st->k_inner + j_in_chunk);
   const double lam = (kk + 1.0) / (kk + 2.0);
   const int64_t j = (int64_t)blockIdx.x * kTile + threadIdx.x;
-  // epilogue operands do not depend on the SpMV: issue their loads first
-  double Cj = 0.0, xj = 0.0, cj = 0.0, lbj = 0.0, ubj = 0.0, x0 = 0.0;
+  // operands of the epilogue do not depend on the SpMV: load them first
+  double xj = 0.0, x0 = 0.0, Dj = 0.0, lb = 0.0, ub = 0.0, cj = 0.0;
   if (j < n) {
-    Cj = V.C[j]; xj = V.x[j]; cj = V.c[j]; lbj = V.lb[j]; ubj = V.ub[j]; x0 = V.x0[j];
+    xj = V.x[j];
+    x0 = (double)V.x0[j];
+    Dj = (double)V.D[j];
+    col_data<DICT>(V.col, j, lb, ub, cj);
   }
-  const double s = (j < n) ? sell_dot<UNIT>(S, j, V.ry) : 0.0;
+  const double s = (j < n) ? sell_dot<UNIT>(S, j, V.y) : 0.0;
   double dx = 0.0, dx0 = 0.0;
   if (j < n) {
-    const double xt = clampd(xj - tau * (cj - Cj * s), lbj, ubj);
-    V.cxb[j] = Cj * (2.0 * xt - xj);
+    const double xt = clampd(xj - tau * Dj * (cj - s), lb, ub);
+    V.xbar[j] = 2.0 * xt - xj;
     V.x[j] = lam * ((1.0 + refl) * xt - refl * xj) + (1.0 - lam) * x0;
     if (CHECK) {
       V.xt[j] = xt;
-      V.cxt[j] = Cj * xt;
-      dx = (xt - xj) * (xt - xj);
-      dx0 = (xt - x0) * (xt - x0);
+      const double w = 1.0 / Dj;
+      dx = (xt - xj) * (xt - xj) * w;
+      dx0 = (xt - x0) * (xt - x0) * w;
     }
   }
   if (CHECK) {
@@ -172,10 +214,10 @@ __global__ void __launch_bounds__(kThreads) col_step_kernel(
   }
 }
 
-// Dual half-step over rows (CSR), fused with A.xbar.
-template <bool UNIT, bool CHECK>
-__global__ void __launch_bounds__(kThreads) row_step_kernel(
-    int32_t m, SellView S, Vecs V, int j_in_chunk) {
+// Dual half-step over rows (CSR as SELL), fused with A.xbar.
+template <bool UNIT, bool DICT, bool CHECK>
+__global__ void __launch_bounds__(kThreads) row_step_kernel(int32_t m, SellView S, Vecs V,
+                                                            int j_in_chunk) {
   __shared__ double sh[32];
   const PdlpState* st = V.st;
   if (st->done) return;
@@ -183,23 +225,24 @@ __global__ void __launch_bounds__(kThreads) row_step_kernel(
   const double kk = (double)(st->k_inner + j_in_chunk);
   const double lam = (kk + 1.0) / (kk + 2.0);
   const int64_t i = (int64_t)blockIdx.x * kTile + threadIdx.x;
-  double Ri = 0.0, yi = 0.0, loi = 0.0, hii = 0.0, y0 = 0.0;
+  double yi = 0.0, y0 = 0.0, Ei = 0.0, lo = 0.0, hi = 0.0;
   if (i < m) {
-    Ri = V.R[i]; yi = V.y[i]; loi = V.lo[i]; hii = V.hi[i]; y0 = V.y0[i];
+    yi = V.y[i];
+    y0 = (double)V.y0[i];
+    Ei = (double)V.E[i];
+    row_data<DICT>(V.row, i, lo, hi);
   }
-  const double s = (i < m) ? sell_dot<UNIT>(S, i, V.cxb) : 0.0;
+  const double s = (i < m) ? sell_dot<UNIT, 8>(S, i, V.xbar) : 0.0;
   double dy = 0.0, dy0 = 0.0;
   if (i < m) {
-    const double v = Ri * s;
-    const double yt = yi - sigma * (v - clampd(v - yi / sigma, loi, hii));
-    const double yn = lam * ((1.0 + refl) * yt - refl * yi) + (1.0 - lam) * y0;
-    V.y[i] = yn;
-    V.ry[i] = Ri * yn;
+    const double se = sigma * Ei;
+    const double yt = yi - se * (s - clampd(s - yi / se, lo, hi));
+    V.y[i] = lam * ((1.0 + refl) * yt - refl * yi) + (1.0 - lam) * y0;
     if (CHECK) {
       V.yt[i] = yt;
-      V.ryt[i] = Ri * yt;
-      dy = (yt - yi) * (yt - yi);
-      dy0 = (yt - y0) * (yt - y0);
+      const double w = 1.0 / Ei;
+      dy = (yt - yi) * (yt - yi) * w;
+      dy0 = (yt - y0) * (yt - y0) * w;
     }
   }
   if (CHECK) {
@@ -210,24 +253,20 @@ __global__ void __launch_bounds__(kThreads) row_step_kernel(
   }
 }
 
-// KKT over rows at T(z): primal residual of A.x_u and the row part of the
-// dual objective.
+// KKT over rows at T(z) = (xt, yt): primal residual of A.xt against the row
+// bounds and the row part of the dual objective.
 template <bool UNIT>
-__global__ void __launch_bounds__(kThreads) kkt_row_kernel(
-    int32_t m, SellView S, Vecs V) {
+__global__ void __launch_bounds__(kThreads) kkt_row_kernel(int32_t m, SellView S, Vecs V) {
   __shared__ double sh[32];
-  const PdlpState* st = V.st;
-  if (st->done) return;
-  const double beta = st->beta, gamma = st->gamma;
+  if (V.st->done) return;
   const int64_t i = (int64_t)blockIdx.x * kTile + threadIdx.x;
-  const double s = (i < m) ? sell_dot<UNIT>(S, i, V.cxt) : 0.0;
+  const double s = (i < m) ? sell_dot<UNIT, 8>(S, i, V.xt) : 0.0;
   double rp = 0.0, dobj = 0.0;
   if (i < m) {
-    const double ax = beta * s;
     const double lo = V.lo_u[i], hi = V.hi_u[i];
-    const double r = ax - clampd(ax, lo, hi);
+    const double r = s - clampd(s, lo, hi);
     rp = r * r;
-    const double yu = gamma * V.ryt[i];
+    const double yu = V.yt[i];
     if (yu > 0.0 && isfinite(lo)) dobj = lo * yu;
     else if (yu < 0.0 && isfinite(hi)) dobj = hi * yu;
   }
@@ -240,25 +279,22 @@ __global__ void __launch_bounds__(kThreads) kkt_row_kernel(
 // KKT over columns: reduced costs, dual residual, primal objective and the
 // bound part of the dual objective.
 template <bool UNIT>
-__global__ void __launch_bounds__(kThreads) kkt_col_kernel(
-    int32_t n, SellView S, Vecs V) {
+__global__ void __launch_bounds__(kThreads) kkt_col_kernel(int32_t n, SellView S, Vecs V) {
   __shared__ double sh[32];
-  const PdlpState* st = V.st;
-  if (st->done) return;
-  const double beta = st->beta, gamma = st->gamma;
+  if (V.st->done) return;
   const int64_t j = (int64_t)blockIdx.x * kTile + threadIdx.x;
-  const double s = (j < n) ? sell_dot<UNIT>(S, j, V.ryt) : 0.0;
+  const double s = (j < n) ? sell_dot<UNIT>(S, j, V.yt) : 0.0;
   double rd = 0.0, pobj = 0.0, dobj = 0.0;
   if (j < n) {
     const double cj = V.c_u[j];
-    const double g = cj - gamma * s;
+    const double g = cj - s;
     const double lb = V.lb_u[j], ub = V.ub_u[j];
     double lamb = 0.0;
     if (g > 0.0 && isfinite(lb)) lamb = g;
     else if (g < 0.0 && isfinite(ub)) lamb = g;
     const double r = g - lamb;
     rd = r * r;
-    pobj = cj * beta * V.cxt[j];
+    pobj = cj * V.xt[j];
     if (lamb > 0.0) dobj = lamb * lb;
     else if (lamb < 0.0) dobj = lamb * ub;
   }
@@ -310,9 +346,9 @@ __global__ void __launch_bounds__(1024) control_kernel(Vecs V) {
     st->have_r0 = 1;
     st->rprev = r;
   }
-  const bool sufficient = r <= 0.2 * st->r0;
-  const bool necessary = r <= 0.8 * st->r0 && r > st->rprev;
-  const bool artificial = (double)st->k_inner >= 0.36 * (double)st->total;
+  const bool sufficient = r <= st->rs_suff * st->r0;
+  const bool necessary = r <= st->rs_nec * st->r0 && r > st->rprev;
+  const bool artificial = (double)st->k_inner >= st->rs_art * (double)st->total;
   st->rprev = r;
   if (sufficient || necessary || artificial) {
     st->restart = 1;
@@ -321,8 +357,7 @@ __global__ void __launch_bounds__(1024) control_kernel(Vecs V) {
     st->have_r0 = 0;
     const double dxr = sqrt(q[Q_DX0]), dyr = sqrt(q[Q_DY0]);
     if (dxr > 1e-10 && dyr > 1e-10) {
-      const double lw = 0.5 * log(dyr / dxr) + 0.5 * log(w);
-      st->omega = exp(lw);
+      st->omega = exp(st->theta * log(dyr / dxr) + (1.0 - st->theta) * log(w));
       st->tau = st->eta / st->omega;
       st->sigma = st->eta * st->omega;
     }
@@ -336,7 +371,7 @@ __global__ void restart_x_kernel(int32_t n, Vecs V) {
        j += (int64_t)gridDim.x * blockDim.x) {
     const double xt = V.xt[j];
     V.x[j] = xt;
-    V.x0[j] = xt;
+    V.x0[j] = (float)xt;
   }
 }
 __global__ void restart_y_kernel(int32_t m, Vecs V) {
@@ -345,15 +380,14 @@ __global__ void restart_y_kernel(int32_t m, Vecs V) {
        i += (int64_t)gridDim.x * blockDim.x) {
     const double yt = V.yt[i];
     V.y[i] = yt;
-    V.y0[i] = yt;
-    V.ry[i] = V.ryt[i];
+    V.y0[i] = (float)yt;
   }
 }
 
 // ---------------------------------------------------------------------------
-// Setup kernels: equilibration statistics, scaled data, power iteration.
+// Setup kernels: equilibration statistics, norms, power iteration.
 
-// stat[r] = max (MAX=true) or sum of |a_rj| * s_j over the row/column
+// stat[r] = max (MAX) or sum of |a_rj| * other_j over the row/column, times self_r
 template <bool UNIT, bool MAX>
 __global__ void abs_stat_kernel(int64_t count, const int64_t* __restrict__ ptr,
                                 const uint32_t* __restrict__ idx, const double* __restrict__ val,
@@ -387,22 +421,16 @@ __global__ void fill_kernel(int64_t count, double* p, double v) {
     p[r] = v;
 }
 
-// Scaled column data: c_s = C c, lb_s = lb / C, ub_s = ub / C (before beta/gamma).
-__global__ void scale_cols_kernel(int32_t n, const double* C, const double* c, const double* lb,
-                                  const double* ub, double* cs, double* lbs, double* ubs,
-                                  double* part) {
-  __shared__ double sh[32];
-  double cc = 0.0;
-  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
-       j += (int64_t)gridDim.x * blockDim.x) {
-    const double Cj = C[j];
-    cs[j] = c[j] * Cj;
-    lbs[j] = lb[j] / Cj;
-    ubs[j] = ub[j] / Cj;
-    cc += cs[j] * cs[j];
+// D = fp32(s^2), root = sqrt(D) (the exact preconditioner the solver uses)
+__global__ void precond_kernel(int64_t count, const double* __restrict__ s, float* __restrict__ D,
+                               double* __restrict__ root) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < count;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    float d = (float)(s[r] * s[r]);
+    if (!(d > 0.0f) || !isfinite(d)) d = 1.0f;
+    D[r] = d;
+    root[r] = sqrt((double)d);
   }
-  double a = block_sum(cc, sh);
-  if (threadIdx.x == 0) part[blockIdx.x] = a;
 }
 
 __device__ __forceinline__ double bound_ref(double lo, double hi) {
@@ -411,23 +439,22 @@ __device__ __forceinline__ double bound_ref(double lo, double hi) {
   return 0.0;
 }
 
-__global__ void scale_rows_kernel(int32_t m, const double* R, const double* lo, const double* hi,
-                                  double* los, double* his, double* part_s, double* part_u) {
+// Norm partials: ||s.c||^2 and ||c||^2 over columns, ||s.b||^2 and ||b||^2 over rows.
+__global__ void norms_kernel(int64_t count, const double* __restrict__ s, const double* __restrict__ a,
+                             const double* __restrict__ b, int is_row, double* part_s,
+                             double* part_u) {
   __shared__ double sh[32];
-  double bs = 0.0, bu = 0.0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const double Ri = R[i];
-    los[i] = lo[i] * Ri;
-    his[i] = hi[i] * Ri;
-    const double b = bound_ref(lo[i], hi[i]);
-    bs += (b * Ri) * (b * Ri);
-    bu += b * b;
+  double ss = 0.0, su = 0.0;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < count;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const double v = is_row ? bound_ref(a[r], b[r]) : a[r];
+    ss += (v * s[r]) * (v * s[r]);
+    su += v * v;
   }
-  double a = block_sum(bs, sh);
-  if (threadIdx.x == 0) part_s[blockIdx.x] = a;
-  a = block_sum(bu, sh);
-  if (threadIdx.x == 0) part_u[blockIdx.x] = a;
+  double t = block_sum(ss, sh);
+  if (threadIdx.x == 0) part_s[blockIdx.x] = t;
+  t = block_sum(su, sh);
+  if (threadIdx.x == 0) part_u[blockIdx.x] = t;
 }
 
 __global__ void sumsq_kernel(int64_t count, const double* v, double* part) {
@@ -446,13 +473,19 @@ __global__ void scale_inplace_kernel(int64_t count, double* v, double s) {
     v[r] *= s;
 }
 
-// out_r = self_r * sum_j a_rj * in_j   (in already carries the other side's scale)
+__global__ void mul_kernel(int64_t count, double* __restrict__ out, const double* __restrict__ a,
+                           const double* __restrict__ b) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < count;
+       r += (int64_t)gridDim.x * blockDim.x)
+    out[r] = a[r] * b[r];
+}
+
+// out_r = self_r * sum_j a_rj * in_j  (CSR/CSC, thread per row)
 template <bool UNIT>
 __global__ void spmv_scaled_kernel(int64_t count, const int64_t* __restrict__ ptr,
                                    const uint32_t* __restrict__ idx, const double* __restrict__ val,
                                    const double* __restrict__ in, const double* __restrict__ self,
-                                   const double* __restrict__ post, double* __restrict__ out,
-                                   double* __restrict__ out_post) {
+                                   double* __restrict__ out) {
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < count;
        r += (int64_t)gridDim.x * blockDim.x) {
     double acc = 0.0;
@@ -465,44 +498,36 @@ __global__ void spmv_scaled_kernel(int64_t count, const int64_t* __restrict__ pt
         acc += val[p] * in[t];
       }
     }
-    const double o = self[r] * acc;
-    out[r] = o;
-    if (out_post) out_post[r] = post[r] * o;
+    out[r] = self ? self[r] * acc : acc;
   }
 }
 
 __global__ void init_iterates_kernel(int32_t n, int32_t m, Vecs V, int warm,
-                                     const double* xin, const double* yin) {
-  const double beta = V.st->beta, gamma = V.st->gamma;
+                                     const double* __restrict__ xin, const double* __restrict__ yin) {
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
        j += (int64_t)gridDim.x * blockDim.x) {
-    double x0 = warm ? xin[j] / (V.C[j] * beta) : 0.0;
-    x0 = clampd(x0, V.lb[j], V.ub[j]);
+    const double x0 = clampd(warm ? xin[j] : 0.0, V.lb_u[j], V.ub_u[j]);
     V.x[j] = x0;
-    V.x0[j] = x0;
+    V.x0[j] = (float)x0;
     V.xt[j] = x0;
-    V.cxt[j] = V.C[j] * x0;
   }
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const double y0 = warm ? yin[i] / (V.R[i] * gamma) : 0.0;
+    const double y0 = warm ? yin[i] : 0.0;
     V.y[i] = y0;
-    V.y0[i] = y0;
+    V.y0[i] = (float)y0;
     V.yt[i] = y0;
-    V.ry[i] = V.R[i] * y0;
-    V.ryt[i] = V.ry[i];
   }
 }
 
-__global__ void unscale_kernel(int32_t n, int32_t m, Vecs V, double* xo, double* yo) {
-  const double beta = V.st->beta, gamma = V.st->gamma;
+__global__ void output_kernel(int32_t n, int32_t m, Vecs V, double* xo, double* yo) {
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
        j += (int64_t)gridDim.x * blockDim.x)
-    xo[j] = clampd(beta * V.cxt[j], V.lb_u[j], V.ub_u[j]);
+    xo[j] = V.xt[j];
   if (yo)
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
          i += (int64_t)gridDim.x * blockDim.x)
-      yo[i] = gamma * V.ryt[i];
+      yo[i] = V.yt[i];
 }
 
 __global__ void hash_fill_kernel(int64_t count, double* v) {
@@ -512,13 +537,6 @@ __global__ void hash_fill_kernel(int64_t count, double* v) {
     h ^= h >> 31; h *= 0xBF58476D1CE4E5B9ull; h ^= h >> 29;
     v[r] = ((double)(h >> 11) * (1.0 / 9007199254740992.0)) - 0.5;
   }
-}
-
-__global__ void mul_kernel(int64_t count, double* __restrict__ out, const double* __restrict__ a,
-                           const double* __restrict__ b) {
-  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < count;
-       r += (int64_t)gridDim.x * blockDim.x)
-    out[r] = a[r] * b[r];
 }
 
 // ---------------------------------------------------------------------------
@@ -540,17 +558,13 @@ struct Workspace {
   }
 };
 
-double host_sum(const std::vector<double>& v) {
-  double a = 0.0;
-  for (double x : v) a += x;
-  return a;
-}
-
 int read_partials(double* dpart, int count, cudaStream_t st, double* out) {
   std::vector<double> h(count);
   TECCL_CUDA(cudaMemcpyAsync(h.data(), dpart, count * sizeof(double), cudaMemcpyDeviceToHost, st));
   TECCL_CUDA(cudaStreamSynchronize(st));
-  *out = host_sum(h);
+  double a = 0.0;
+  for (double x : h) a += x;
+  *out = a;
   return TECCL_OK;
 }
 
@@ -560,32 +574,29 @@ SellView row_view(const teccl_lp* lp) {
 SellView col_view(const teccl_lp* lp) {
   return SellView{lp->scol_off, lp->scol_w, lp->scol_idx, lp->scol_val, lp->n};
 }
-template <bool UNIT, bool CHECK>
+
+template <bool UNIT, bool DICT, bool CHECK>
 void launch_col(cudaStream_t st, const teccl_lp* lp, const Vecs& V, int j) {
-  col_step_kernel<UNIT, CHECK><<<V.nb_col, kThreads, 0, st>>>(lp->n, col_view(lp), V, j);
+  col_step_kernel<UNIT, DICT, CHECK><<<V.nb_col, kThreads, 0, st>>>(lp->n, col_view(lp), V, j);
 }
-template <bool UNIT, bool CHECK>
+template <bool UNIT, bool DICT, bool CHECK>
 void launch_row(cudaStream_t st, const teccl_lp* lp, const Vecs& V, int j) {
-  row_step_kernel<UNIT, CHECK><<<V.nb_row, kThreads, 0, st>>>(lp->m, row_view(lp), V, j);
-}
-template <bool UNIT>
-void launch_kkt(cudaStream_t st, const teccl_lp* lp, const Vecs& V) {
-  kkt_row_kernel<UNIT><<<V.nb_row, kThreads, 0, st>>>(lp->m, row_view(lp), V);
-  kkt_col_kernel<UNIT><<<V.nb_col, kThreads, 0, st>>>(lp->n, col_view(lp), V);
+  row_step_kernel<UNIT, DICT, CHECK><<<V.nb_row, kThreads, 0, st>>>(lp->m, row_view(lp), V, j);
 }
 
-template <bool UNIT>
+template <bool UNIT, bool DICT>
 void enqueue_chunk(int chunk, cudaStream_t st, const teccl_lp* lp, const Vecs& V) {
   for (int j = 0; j < chunk; ++j) {
     if (j == chunk - 1) {
-      launch_col<UNIT, true>(st, lp, V, j);
-      launch_row<UNIT, true>(st, lp, V, j);
+      launch_col<UNIT, DICT, true>(st, lp, V, j);
+      launch_row<UNIT, DICT, true>(st, lp, V, j);
     } else {
-      launch_col<UNIT, false>(st, lp, V, j);
-      launch_row<UNIT, false>(st, lp, V, j);
+      launch_col<UNIT, DICT, false>(st, lp, V, j);
+      launch_row<UNIT, DICT, false>(st, lp, V, j);
     }
   }
-  launch_kkt<UNIT>(st, lp, V);
+  kkt_row_kernel<UNIT><<<V.nb_row, kThreads, 0, st>>>(lp->m, row_view(lp), V);
+  kkt_col_kernel<UNIT><<<V.nb_col, kThreads, 0, st>>>(lp->n, col_view(lp), V);
   control_kernel<<<1, 1024, 0, st>>>(V);
   restart_x_kernel<<<grid_for(lp->n), kThreads, 0, st>>>(lp->n, V);
   restart_y_kernel<<<grid_for(lp->m), kThreads, 0, st>>>(lp->m, V);
@@ -594,12 +605,11 @@ void enqueue_chunk(int chunk, cudaStream_t st, const teccl_lp* lp, const Vecs& V
 struct StepBench {
   int reps;
   double ms_col, ms_row, bytes_col, bytes_row;
-  int gs_col, gs_row;
 };
 
-template <bool UNIT>
+template <bool UNIT, bool DICT>
 int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x_dev,
-               double* y_dev, teccl_pdlp_result* res, StepBench* sb = nullptr) {
+               double* y_dev, teccl_pdlp_result* res, StepBench* sb) {
   cudaStream_t st = ctx->stream;
   const int32_t m = lp->m, n = lp->n;
   Workspace W;
@@ -610,116 +620,128 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
   TECCL_CUDA(cudaEventRecord(ev0, st));
   auto t_start = std::chrono::steady_clock::now();
 
-  double *R = W.alloc<double>(m), *C = W.alloc<double>(n), *rstat = W.alloc<double>(m),
-         *cstat = W.alloc<double>(n);
-  double *cs = W.alloc<double>(n), *lbs = W.alloc<double>(n), *ubs = W.alloc<double>(n);
-  double *los = W.alloc<double>(m), *his = W.alloc<double>(m);
-  // gathered vectors (cxb, cxt, ry, ryt) carry one extra always-zero slot:
-  // the SELL padding entries point at it
-  double *x = W.alloc<double>(n), *x0 = W.alloc<double>(n), *xt = W.alloc<double>(n),
-         *cxb = W.alloc<double>(n + 1), *cxt = W.alloc<double>(n + 1);
-  double *y = W.alloc<double>(m), *y0 = W.alloc<double>(m), *yt = W.alloc<double>(m),
-         *ry = W.alloc<double>(m + 1), *ryt = W.alloc<double>(m + 1);
   const int nb_row = (int)((m + kTile - 1) / kTile), nb_col = (int)((n + kTile - 1) / kTile);
   const int64_t pstride = std::max<int64_t>(std::max(nb_row, nb_col), kGrid);
+  double *R = W.alloc<double>(m + 1), *C = W.alloc<double>(n + 1), *rstat = W.alloc<double>(m),
+         *cstat = W.alloc<double>(n);
+  float *D = W.alloc<float>(n), *E = W.alloc<float>(m);
+  float *x0 = W.alloc<float>(n), *y0 = W.alloc<float>(m);
+  double *x = W.alloc<double>(n), *xt = W.alloc<double>(n + 1), *xbar = W.alloc<double>(n + 1);
+  double *y = W.alloc<double>(m + 1), *yt = W.alloc<double>(m + 1);
   double* part = W.alloc<double>((int64_t)kNQ * pstride);
   double* part2 = W.alloc<double>(kGrid);
   PdlpState* dst = W.alloc<PdlpState>(1);
-  if (!R || !C || !rstat || !cstat || !cs || !lbs || !ubs || !los || !his || !x || !x0 || !xt ||
-      !cxb || !cxt || !y || !y0 || !yt || !ry || !ryt || !part || !part2 || !dst) {
+  if (!R || !C || !rstat || !cstat || !D || !E || !x0 || !y0 || !x || !xt || !xbar || !y || !yt ||
+      !part || !part2 || !dst) {
     set_error("device allocation failed for PDLP workspace");
     return TECCL_ENOMEM;
   }
   TECCL_CUDA(cudaMemsetAsync(part, 0, sizeof(double) * kNQ * pstride, st));
-  TECCL_CUDA(cudaMemsetAsync(cxb, 0, sizeof(double) * (n + 1), st));
-  TECCL_CUDA(cudaMemsetAsync(cxt, 0, sizeof(double) * (n + 1), st));
-  TECCL_CUDA(cudaMemsetAsync(ry, 0, sizeof(double) * (m + 1), st));
-  TECCL_CUDA(cudaMemsetAsync(ryt, 0, sizeof(double) * (m + 1), st));
+  // always-zero slots the SELL padding gathers from
+  TECCL_CUDA(cudaMemsetAsync(xt, 0, sizeof(double) * (n + 1), st));
+  TECCL_CUDA(cudaMemsetAsync(xbar, 0, sizeof(double) * (n + 1), st));
+  TECCL_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * (m + 1), st));
+  TECCL_CUDA(cudaMemsetAsync(yt, 0, sizeof(double) * (m + 1), st));
   {
     int rc = teccl_build_sell(lp, st);
     if (rc) return rc;
   }
   const int gr = grid_for(m > n ? m : n);
+  int64_t nl = 0;  // kernel launches issued by this solve
 
-  // --- Ruiz equilibration + Pock-Chambolle (alpha = 1), simultaneous updates.
+  // --- Ruiz equilibration + Pock-Chambolle (alpha = 1), simultaneous updates
   fill_kernel<<<gr, kThreads, 0, st>>>(m, R, 1.0);
   fill_kernel<<<gr, kThreads, 0, st>>>(n, C, 1.0);
-  for (int it = 0; it < o->ruiz_iters; ++it) {
-    abs_stat_kernel<UNIT, true><<<gr, kThreads, 0, st>>>(m, lp->row_ptr, lp->col, lp->val, C, R, rstat);
-    abs_stat_kernel<UNIT, true><<<gr, kThreads, 0, st>>>(n, lp->col_ptr, lp->row, lp->cval, R, C, cstat);
+  nl += 2;
+  for (int it = 0; it <= o->ruiz_iters; ++it) {
+    if (it < o->ruiz_iters) {
+      abs_stat_kernel<UNIT, true><<<gr, kThreads, 0, st>>>(m, lp->row_ptr, lp->col, lp->val, C, R, rstat);
+      abs_stat_kernel<UNIT, true><<<gr, kThreads, 0, st>>>(n, lp->col_ptr, lp->row, lp->cval, R, C, cstat);
+    } else {
+      abs_stat_kernel<UNIT, false><<<gr, kThreads, 0, st>>>(m, lp->row_ptr, lp->col, lp->val, C, R, rstat);
+      abs_stat_kernel<UNIT, false><<<gr, kThreads, 0, st>>>(n, lp->col_ptr, lp->row, lp->cval, R, C, cstat);
+    }
     apply_scale_kernel<<<gr, kThreads, 0, st>>>(m, R, rstat);
     apply_scale_kernel<<<gr, kThreads, 0, st>>>(n, C, cstat);
+    nl += 4;
   }
-  abs_stat_kernel<UNIT, false><<<gr, kThreads, 0, st>>>(m, lp->row_ptr, lp->col, lp->val, C, R, rstat);
-  abs_stat_kernel<UNIT, false><<<gr, kThreads, 0, st>>>(n, lp->col_ptr, lp->row, lp->cval, R, C, cstat);
-  apply_scale_kernel<<<gr, kThreads, 0, st>>>(m, R, rstat);
-  apply_scale_kernel<<<gr, kThreads, 0, st>>>(n, C, cstat);
   TECCL_CHECK_LAUNCH();
 
-  // --- scaled data and the bound/objective rescaling
-  scale_cols_kernel<<<kGrid, kThreads, 0, st>>>(n, C, lp->obj, lp->var_lb, lp->var_ub, cs, lbs, ubs, part);
-  double csq = 0.0;
-  if (read_partials(part, kGrid, st, &csq)) return TECCL_ECUDA;
-  scale_rows_kernel<<<kGrid, kThreads, 0, st>>>(m, R, lp->row_lo, lp->row_hi, los, his, part, part2);
-  double bsq = 0.0, bsq_u = 0.0;
-  if (read_partials(part, kGrid, st, &bsq)) return TECCL_ECUDA;
-  if (read_partials(part2, kGrid, st, &bsq_u)) return TECCL_ECUDA;
-  sumsq_kernel<<<kGrid, kThreads, 0, st>>>(n, lp->obj, part);
-  double csq_u = 0.0;
-  if (read_partials(part, kGrid, st, &csq_u)) return TECCL_ECUDA;
-  const double beta = sqrt(bsq) + 1.0, gamma = sqrt(csq) + 1.0;
-  scale_inplace_kernel<<<gr, kThreads, 0, st>>>(n, cs, 1.0 / gamma);
-  scale_inplace_kernel<<<gr, kThreads, 0, st>>>(n, lbs, 1.0 / beta);
-  scale_inplace_kernel<<<gr, kThreads, 0, st>>>(n, ubs, 1.0 / beta);
-  scale_inplace_kernel<<<gr, kThreads, 0, st>>>(m, los, 1.0 / beta);
-  scale_inplace_kernel<<<gr, kThreads, 0, st>>>(m, his, 1.0 / beta);
-  TECCL_CHECK_LAUNCH();
+  // --- preconditioners (fp32, exact from here on) and their square roots
+  double* rootE = rstat;
+  double* rootD = cstat;
+  precond_kernel<<<gr, kThreads, 0, st>>>(m, R, E, rootE);
+  precond_kernel<<<gr, kThreads, 0, st>>>(n, C, D, rootD);
+  nl += 2;
 
-  // --- power iteration for ||A_s||_2: v in xt, C.v in cxt, A_s.v in yt, R.A_s.v in ryt
+  // --- norms: scaled ||C c||, ||R b|| set the initial primal weight (the
+  // bound/objective rescaling of PDLP); unscaled ||c||, ||b|| enter the
+  // relative termination criteria
+  double csq_s = 0.0, csq_u = 0.0, bsq_s = 0.0, bsq_u = 0.0;
+  norms_kernel<<<kGrid, kThreads, 0, st>>>(n, C, lp->obj, nullptr, 0, part, part2);
+  if (read_partials(part, kGrid, st, &csq_s) || read_partials(part2, kGrid, st, &csq_u)) return TECCL_ECUDA;
+  norms_kernel<<<kGrid, kThreads, 0, st>>>(m, R, lp->row_lo, lp->row_hi, 1, part, part2);
+  if (read_partials(part, kGrid, st, &bsq_s) || read_partials(part2, kGrid, st, &bsq_u)) return TECCL_ECUDA;
+  nl += 2;
+  const double beta = sqrt(bsq_s) + 1.0, gamma = sqrt(csq_s) + 1.0;
+  const double cn_s = sqrt(csq_s) / gamma, bn_s = sqrt(bsq_s) / beta;
+  const double omega_s = (cn_s > 1e-10 && bn_s > 1e-10) ? cn_s / bn_s : 1.0;
+
+  // --- power iteration for ||E^1/2 A D^1/2||_2 (v in xt, D^1/2 v in xbar,
+  // A D^1/2 v in yt, E A D^1/2 v in y)
   double sigma_max = 1.0;
-  int64_t nl = 2 + 4LL * o->ruiz_iters + 4 + 1 + 1 + 1 + 5;  // kernel launches so far
   if (m > 0 && n > 0 && lp->nnz > 0) {
-    nl += 3;
     hash_fill_kernel<<<gr, kThreads, 0, st>>>(n, xt);
     double nv = 0.0;
     sumsq_kernel<<<kGrid, kThreads, 0, st>>>(n, xt, part);
     if (read_partials(part, kGrid, st, &nv)) return TECCL_ECUDA;
     scale_inplace_kernel<<<gr, kThreads, 0, st>>>(n, xt, 1.0 / sqrt(nv));
+    nl += 3;
     for (int it = 0; it < 40; ++it) {
-      mul_kernel<<<gr, kThreads, 0, st>>>(n, cxt, xt, C);
-      spmv_scaled_kernel<UNIT><<<gr, kThreads, 0, st>>>(m, lp->row_ptr, lp->col, lp->val, cxt, R, R, yt, ryt);
-      spmv_scaled_kernel<UNIT><<<gr, kThreads, 0, st>>>(n, lp->col_ptr, lp->row, lp->cval, ryt, C, nullptr, xt, nullptr);
+      mul_kernel<<<gr, kThreads, 0, st>>>(n, xbar, xt, rootD);
+      spmv_scaled_kernel<UNIT><<<gr, kThreads, 0, st>>>(m, lp->row_ptr, lp->col, lp->val, xbar, nullptr, yt);
+      mul_kernel<<<gr, kThreads, 0, st>>>(m, y, yt, rootE);
+      mul_kernel<<<gr, kThreads, 0, st>>>(m, y, y, rootE);
+      spmv_scaled_kernel<UNIT><<<gr, kThreads, 0, st>>>(n, lp->col_ptr, lp->row, lp->cval, y, rootD, xt);
       sumsq_kernel<<<kGrid, kThreads, 0, st>>>(n, xt, part);
-      nl += 5;
+      nl += 6;
       if (read_partials(part, kGrid, st, &nv)) return TECCL_ECUDA;
       if (!(nv > 0.0)) break;
       scale_inplace_kernel<<<gr, kThreads, 0, st>>>(n, xt, 1.0 / sqrt(nv));
+      nl += 1;
     }
     if (nv > 0.0) sigma_max = sqrt(sqrt(nv));
+    TECCL_CUDA(cudaMemsetAsync(xbar, 0, sizeof(double) * (n + 1), st));
+    TECCL_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * (m + 1), st));
+    TECCL_CUDA(cudaMemsetAsync(xt, 0, sizeof(double) * (n + 1), st));
+    TECCL_CUDA(cudaMemsetAsync(yt, 0, sizeof(double) * (m + 1), st));
   }
   TECCL_CHECK_LAUNCH();
 
-  // --- state
+  // --- state: omega in original space = scaled weight * gamma / beta
   PdlpState hs{};
   hs.eta = 0.998 / sigma_max;
-  const double cn_s = sqrt(csq) / gamma, bn_s = sqrt(bsq) / beta;
-  hs.omega = (cn_s > 1e-10 && bn_s > 1e-10) ? cn_s / bn_s : 1.0;
+  hs.omega = omega_s * gamma / beta;
   hs.tau = hs.eta / hs.omega;
   hs.sigma = hs.eta * hs.omega;
   hs.refl = o->reflection;
-  hs.beta = beta;
-  hs.gamma = gamma;
   hs.bnorm = sqrt(bsq_u);
   hs.cnorm = sqrt(csq_u);
   hs.eps = o->eps_rel;
+  hs.rs_suff = o->restart_sufficient;
+  hs.rs_nec = o->restart_necessary;
+  hs.rs_art = o->restart_artificial;
+  hs.theta = o->omega_theta;
   const int chunk = o->check_every > 0 ? o->check_every : 64;
   hs.chunk_len = chunk;
   TECCL_CUDA(cudaMemcpyAsync(dst, &hs, sizeof(hs), cudaMemcpyHostToDevice, st));
 
   Vecs V{};
-  V.c = cs; V.lb = lbs; V.ub = ubs; V.lo = los; V.hi = his; V.R = R; V.C = C;
-  V.x = x; V.x0 = x0; V.xt = xt; V.cxb = cxb; V.cxt = cxt;
-  V.y = y; V.y0 = y0; V.yt = yt; V.ry = ry; V.ryt = ryt;
+  V.D = D; V.E = E;
+  V.col = Bounds{lp->col_code, lp->col_dict, lp->var_lb, lp->var_ub, lp->obj};
+  V.row = Bounds{lp->row_code, lp->row_dict, lp->row_lo, lp->row_hi, nullptr};
+  V.x = x; V.xt = xt; V.xbar = xbar; V.x0 = x0;
+  V.y = y; V.yt = yt; V.y0 = y0;
   V.c_u = lp->obj; V.lb_u = lp->var_lb; V.ub_u = lp->var_ub; V.lo_u = lp->row_lo; V.hi_u = lp->row_hi;
   V.part = part;
   V.pstride = pstride;
@@ -727,9 +749,8 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
   V.nb_col = nb_col;
   V.st = dst;
   init_iterates_kernel<<<gr, kThreads, 0, st>>>(n, m, V, o->warm_start, x_dev, y_dev);
+  nl += 1;
   TECCL_CHECK_LAUNCH();
-
-  const int gsr = kTile, gsc = kTile;
 
   if (sb) {  // time the fused iteration kernels alone, CUDA events on this stream
     cudaEvent_t a, b, c2;
@@ -737,13 +758,13 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
     TECCL_CUDA(cudaEventCreate(&b));
     TECCL_CUDA(cudaEventCreate(&c2));
     for (int w = 0; w < 3; ++w) {
-      launch_col<UNIT, false>(st, lp, V, 0);
-      launch_row<UNIT, false>(st, lp, V, 0);
+      launch_col<UNIT, DICT, false>(st, lp, V, 0);
+      launch_row<UNIT, DICT, false>(st, lp, V, 0);
     }
     TECCL_CUDA(cudaEventRecord(a, st));
-    for (int r = 0; r < sb->reps; ++r) launch_col<UNIT, false>(st, lp, V, 0);
+    for (int r = 0; r < sb->reps; ++r) launch_col<UNIT, DICT, false>(st, lp, V, 0);
     TECCL_CUDA(cudaEventRecord(b, st));
-    for (int r = 0; r < sb->reps; ++r) launch_row<UNIT, false>(st, lp, V, 0);
+    for (int r = 0; r < sb->reps; ++r) launch_row<UNIT, DICT, false>(st, lp, V, 0);
     TECCL_CUDA(cudaEventRecord(c2, st));
     TECCL_CHECK_LAUNCH();
     TECCL_CUDA(cudaEventSynchronize(c2));
@@ -752,17 +773,15 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
     TECCL_CUDA(cudaEventElapsedTime(&m2, b, c2));
     sb->ms_col = m1 / sb->reps;
     sb->ms_row = m2 / sb->reps;
+    // algorithmic bytes: SELL slice headers and every
+    // stored entry once, the gathered vector once, dense operands once
     const double ib = UNIT ? 4.0 : 12.0;
-    // algorithmic bytes: index stream once, pointer
-    // array once, gathered vector once, 6 dense reads + 2 writes per column,
-    // 5 dense reads + 2 writes per row
-    // SELL-32: slice offsets + widths (12 B per 32 rows), every stored entry
-    // (padding included) once, gathered vector once, dense operands
-    const double ns_c = (n + 31) / 32, ns_r = (m + 31) / 32;
-    sb->bytes_col = 12.0 * ns_c + ib * lp->scol_entries + 8.0 * m + 64.0 * n;
-    sb->bytes_row = 12.0 * ns_r + ib * lp->srow_entries + 8.0 * n + 56.0 * m;
-    sb->gs_col = gsc;
-    sb->gs_row = gsr;
+    const double ns_c = (double)((n + 31) / 32), ns_r = (double)((m + 31) / 32);
+    const double cb = DICT ? 2.0 : 24.0, rbd = DICT ? 2.0 : 16.0;
+    // column: x(8) x0(4) D(4) bounds(cb) read; x(8) xbar(8) written
+    sb->bytes_col = 12.0 * ns_c + ib * lp->scol_entries + 8.0 * m + (32.0 + cb) * n;
+    // row: y(8) y0(4) E(4) bounds(rbd) read; y(8) written
+    sb->bytes_row = 12.0 * ns_r + ib * lp->srow_entries + 8.0 * n + (24.0 + rbd) * m;
     cudaEventDestroy(a); cudaEventDestroy(b); cudaEventDestroy(c2);
     return TECCL_OK;
   }
@@ -774,14 +793,14 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
     cudaStream_t cap;
     TECCL_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
     TECCL_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
-    enqueue_chunk<UNIT>(chunk, cap, lp, V);
+    enqueue_chunk<UNIT, DICT>(chunk, cap, lp, V);
     TECCL_CUDA(cudaStreamEndCapture(cap, &g));
     TECCL_CUDA(cudaGraphInstantiate(&gexec, g, 0));
     TECCL_CUDA(cudaGraphDestroy(g));
     TECCL_CUDA(cudaStreamDestroy(cap));
   }
 
-  // --- iterate: chunks queued `lookahead` deep; the device stops itself.
+  // --- iterate: chunks queued `lookahead` deep; the device stops itself
   const int look = o->lookahead > 0 ? o->lookahead : 1;
   PdlpState* ring = nullptr;
   TECCL_CUDA(cudaMallocHost((void**)&ring, sizeof(PdlpState) * look));
@@ -792,13 +811,12 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
   PdlpState last = hs;
   const int64_t max_chunks = (o->max_iters + chunk - 1) / chunk;
   bool stop = false;
-  int64_t checks_seen = 0;
   while (!stop) {
     while (launched < max_chunks && launched - polled < look) {
       if (gexec) {
         TECCL_CUDA(cudaGraphLaunch(gexec, st));
       } else {
-        enqueue_chunk<UNIT>(chunk, st, lp, V);
+        enqueue_chunk<UNIT, DICT>(chunk, st, lp, V);
       }
       TECCL_CHECK_LAUNCH();
       const int slot = (int)(launched % look);
@@ -811,29 +829,30 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
     TECCL_CUDA(cudaEventSynchronize(evs[slot]));
     last = ring[slot];
     ++polled;
-    ++checks_seen;
-    if (o->verbose > 0 && (checks_seen % o->verbose == 0 || last.done))
+    if (o->verbose > 0 && (polled % o->verbose == 0 || last.done))
       fprintf(stderr, "[teccl pdlp] it=%lld rp=%.2e rd=%.2e gap=%.2e pobj=%.9g w=%.3e r=%.2e restarts=%d\n",
-              last.total, last.rel_p, last.rel_d, last.gap, last.pobj, last.omega, last.last_r, last.restarts);
+              last.total, last.rel_p, last.rel_d, last.gap, last.pobj, last.omega, last.last_r,
+              last.restarts);
     if (last.done == 1) { status = TECCL_OPTIMAL; stop = true; }
     else if (last.done == 2) { status = TECCL_NUMERICAL; stop = true; }
     else if (polled >= max_chunks) { status = TECCL_ITER_LIMIT; stop = true; }
     else {
-      double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+      const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
       if (el > o->time_limit) { status = TECCL_TIME_LIMIT; stop = true; }
     }
   }
-  // stop anything still queued from touching the iterates
   if (status != TECCL_OPTIMAL && status != TECCL_NUMERICAL) {
-    int one = 3;
-    TECCL_CUDA(cudaMemcpyAsync(&dst->done, &one, sizeof(int), cudaMemcpyHostToDevice, st));
+    // stop anything still queued from touching the iterates
+    static const int kStopped = 3;
+    TECCL_CUDA(cudaMemcpyAsync(&dst->done, &kStopped, sizeof(int), cudaMemcpyHostToDevice, st));
   }
   TECCL_CUDA(cudaStreamSynchronize(st));
   TECCL_CUDA(cudaMemcpy(&last, dst, sizeof(PdlpState), cudaMemcpyDeviceToHost));
   if (last.done == 1) status = TECCL_OPTIMAL;
   if (last.done == 3) last.done = 0;
 
-  unscale_kernel<<<gr, kThreads, 0, st>>>(n, m, V, x_dev, y_dev);
+  output_kernel<<<gr, kThreads, 0, st>>>(n, m, V, x_dev, y_dev);
+  nl += 1;
   TECCL_CHECK_LAUNCH();
   TECCL_CUDA(cudaEventRecord(ev1, st));
   TECCL_CUDA(cudaEventSynchronize(ev1));
@@ -856,8 +875,18 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
   res->solve_seconds = ms * 1e-3;
   res->omega = last.omega;
   res->step = hs.eta;
-  res->spmv_launches = nl + 1 + 1 + launched * (2LL * chunk + 5);  // + init + unscale
+  res->spmv_launches = nl + launched * (2LL * chunk + 5);
   return TECCL_OK;
+}
+
+int dispatch(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x_dev, double* y_dev,
+             teccl_pdlp_result* res, StepBench* sb) {
+  const bool dict = lp->col_code && lp->row_code;
+  if (lp->unit)
+    return dict ? solve_impl<true, true>(ctx, lp, o, x_dev, y_dev, res, sb)
+                : solve_impl<true, false>(ctx, lp, o, x_dev, y_dev, res, sb);
+  return dict ? solve_impl<false, true>(ctx, lp, o, x_dev, y_dev, res, sb)
+              : solve_impl<false, false>(ctx, lp, o, x_dev, y_dev, res, sb);
 }
 
 }  // namespace teccl
@@ -875,6 +904,10 @@ extern "C" void teccl_pdlp_default_opts(teccl_pdlp_opts* o) {
   o->reflection = 1.0;
   o->use_graphs = 1;
   o->warm_start = 0;
+  o->restart_sufficient = 0.2;
+  o->restart_necessary = 0.8;
+  o->restart_artificial = 0.36;
+  o->omega_theta = 0.5;
 }
 
 extern "C" int teccl_pdlp_solve_dev(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* opts,
@@ -887,8 +920,7 @@ extern "C" int teccl_pdlp_solve_dev(teccl_ctx* ctx, teccl_lp* lp, const teccl_pd
   TECCL_CUDA(cudaSetDevice(ctx->device));
   *res = teccl_pdlp_result{};
   if (lp->n == 0) { res->status = TECCL_OPTIMAL; return TECCL_OK; }
-  return lp->unit ? solve_impl<true>(ctx, lp, &o, x_dev, y_dev, res)
-                  : solve_impl<false>(ctx, lp, &o, x_dev, y_dev, res);
+  return dispatch(ctx, lp, &o, x_dev, y_dev, res, nullptr);
 }
 
 extern "C" int teccl_pdlp_solve(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* opts,
@@ -916,32 +948,46 @@ extern "C" int teccl_pdlp_solve(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_o
   return rc;
 }
 
+extern "C" int teccl_pdlp_step_bench(teccl_ctx* ctx, teccl_lp* lp, int32_t reps, double* out6) {
+  if (!ctx || !lp || reps < 1 || !out6) { set_error("bad argument"); return TECCL_EINVAL; }
+  TECCL_CUDA(cudaSetDevice(ctx->device));
+  teccl_pdlp_opts o;
+  teccl_pdlp_default_opts(&o);
+  teccl_pdlp_result res{};
+  double* xd = nullptr;
+  TECCL_CUDA(cudaMallocAsync((void**)&xd, sizeof(double) * (lp->n + 1), ctx->stream));
+  StepBench sb{reps, 0, 0, 0, 0};
+  int rc = dispatch(ctx, lp, &o, xd, nullptr, &res, &sb);
+  cudaFreeAsync(xd, ctx->stream);
+  TECCL_CUDA(cudaStreamSynchronize(ctx->stream));
+  out6[0] = sb.ms_col; out6[1] = sb.ms_row; out6[2] = sb.bytes_col; out6[3] = sb.bytes_row;
+  out6[4] = (lp->col_code && lp->row_code) ? 1.0 : 0.0;  // bounds via class dictionaries
+  out6[5] = (double)kSlice;
+  return rc;
+}
+
 extern "C" int teccl_spmv_bench(teccl_ctx* ctx, teccl_lp* lp, int32_t reps, double* ms_per_pair,
                                 double* bytes_per_pair) {
   if (!ctx || !lp || reps < 1) { set_error("bad argument"); return TECCL_EINVAL; }
   cudaStream_t st = ctx->stream;
   TECCL_CUDA(cudaSetDevice(ctx->device));
   const int32_t m = lp->m, n = lp->n;
-  double *vx = nullptr, *vy = nullptr, *ones_m = nullptr, *ones_n = nullptr;
+  double *vx = nullptr, *vy = nullptr;
   TECCL_CUDA(cudaMallocAsync((void**)&vx, sizeof(double) * (n + 1), st));
   TECCL_CUDA(cudaMallocAsync((void**)&vy, sizeof(double) * (m + 1), st));
-  TECCL_CUDA(cudaMallocAsync((void**)&ones_m, sizeof(double) * (m + 1), st));
-  TECCL_CUDA(cudaMallocAsync((void**)&ones_n, sizeof(double) * (n + 1), st));
   const int gr = grid_for(m > n ? m : n);
   hash_fill_kernel<<<gr, kThreads, 0, st>>>(n, vx);
-  fill_kernel<<<gr, kThreads, 0, st>>>(m, ones_m, 1.0);
-  fill_kernel<<<gr, kThreads, 0, st>>>(n, ones_n, 1.0);
   cudaEvent_t a, b;
   TECCL_CUDA(cudaEventCreate(&a));
   TECCL_CUDA(cudaEventCreate(&b));
   for (int it = -3; it < reps; ++it) {
     if (it == 0) TECCL_CUDA(cudaEventRecord(a, st));
     if (lp->unit) {
-      spmv_scaled_kernel<true><<<gr, kThreads, 0, st>>>(m, lp->row_ptr, lp->col, lp->val, vx, ones_m, nullptr, vy, nullptr);
-      spmv_scaled_kernel<true><<<gr, kThreads, 0, st>>>(n, lp->col_ptr, lp->row, lp->cval, vy, ones_n, nullptr, vx, nullptr);
+      spmv_scaled_kernel<true><<<gr, kThreads, 0, st>>>(m, lp->row_ptr, lp->col, lp->val, vx, nullptr, vy);
+      spmv_scaled_kernel<true><<<gr, kThreads, 0, st>>>(n, lp->col_ptr, lp->row, lp->cval, vy, nullptr, vx);
     } else {
-      spmv_scaled_kernel<false><<<gr, kThreads, 0, st>>>(m, lp->row_ptr, lp->col, lp->val, vx, ones_m, nullptr, vy, nullptr);
-      spmv_scaled_kernel<false><<<gr, kThreads, 0, st>>>(n, lp->col_ptr, lp->row, lp->cval, vy, ones_n, nullptr, vx, nullptr);
+      spmv_scaled_kernel<false><<<gr, kThreads, 0, st>>>(m, lp->row_ptr, lp->col, lp->val, vx, nullptr, vy);
+      spmv_scaled_kernel<false><<<gr, kThreads, 0, st>>>(n, lp->col_ptr, lp->row, lp->cval, vy, nullptr, vx);
     }
   }
   TECCL_CHECK_LAUNCH();
@@ -951,30 +997,11 @@ extern "C" int teccl_spmv_bench(teccl_ctx* ctx, teccl_lp* lp, int32_t reps, doub
   TECCL_CUDA(cudaEventElapsedTime(&ms, a, b));
   *ms_per_pair = ms / reps;
   const double vb = lp->unit ? 4.0 : 12.0;
-  // per pair: both index streams, ptr arrays, one dense read of each input
-  // vector (gathers at best once), one write of each output
   *bytes_per_pair = 2.0 * lp->nnz * vb + 8.0 * (m + 1) + 8.0 * (n + 1) + 2.0 * 8.0 * (m + n);
   cudaEventDestroy(a);
   cudaEventDestroy(b);
-  cudaFreeAsync(vx, st); cudaFreeAsync(vy, st); cudaFreeAsync(ones_m, st); cudaFreeAsync(ones_n, st);
+  cudaFreeAsync(vx, st);
+  cudaFreeAsync(vy, st);
   TECCL_CUDA(cudaStreamSynchronize(st));
   return TECCL_OK;
-}
-
-extern "C" int teccl_pdlp_step_bench(teccl_ctx* ctx, teccl_lp* lp, int32_t reps, double* out6) {
-  if (!ctx || !lp || reps < 1 || !out6) { set_error("bad argument"); return TECCL_EINVAL; }
-  TECCL_CUDA(cudaSetDevice(ctx->device));
-  teccl_pdlp_opts o;
-  teccl_pdlp_default_opts(&o);
-  teccl_pdlp_result res{};
-  double* xd = nullptr;
-  TECCL_CUDA(cudaMallocAsync((void**)&xd, sizeof(double) * (lp->n + 1), ctx->stream));
-  StepBench sb{reps, 0, 0, 0, 0, 0, 0};
-  int rc = lp->unit ? solve_impl<true>(ctx, lp, &o, xd, nullptr, &res, &sb)
-                    : solve_impl<false>(ctx, lp, &o, xd, nullptr, &res, &sb);
-  cudaFreeAsync(xd, ctx->stream);
-  TECCL_CUDA(cudaStreamSynchronize(ctx->stream));
-  out6[0] = sb.ms_col; out6[1] = sb.ms_row; out6[2] = sb.bytes_col; out6[3] = sb.bytes_row;
-  out6[4] = sb.gs_col; out6[5] = sb.gs_row;
-  return rc;
 }

@@ -15,6 +15,7 @@
 
 #include <cub/device/device_scan.cuh>
 
+#include <algorithm>
 #include <cmath>
 #include <vector>
 
@@ -45,6 +46,11 @@ struct TeDev {
   const uint32_t* inc;   // edge id | bit31 when the edge leaves the node
   const int* out_ptr;    // [Nn+1] out-edges of node (edge order)
   const int* out_e;
+  // bound-class codes (pdlp.cu dictionaries)
+  int dict_col, dict_row, nU, nOU, nCap;
+  const int* pair_uidx;  // [P] index of the pair's units in the distinct-units list
+  const int* src_ouidx;  // [S] index of the source's out-units in its list
+  const uint16_t* cap_idx;  // [E*K] index of the capacity in the distinct-caps list
 };
 
 __device__ __forceinline__ int64_t varF(const TeDev& d, int s, int e, int k) {
@@ -79,23 +85,27 @@ struct Emitter {
 template <bool FILL>
 __global__ void te_rows_kernel(TeDev d, const int64_t* __restrict__ row_ptr,
                                uint32_t* __restrict__ col, int64_t* __restrict__ row_len,
-                               double* __restrict__ lo, double* __restrict__ hi) {
+                               double* __restrict__ lo, double* __restrict__ hi,
+                               uint16_t* __restrict__ code) {
   const int K = d.K;
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < d.n_rows;
        r += (int64_t)gridDim.x * blockDim.x) {
     Emitter<FILL> em{FILL ? col + row_ptr[r] : nullptr, 0};
     double rlo = 0.0, rhi = 0.0;
+    int rc = 0;                                      // bound class: 0 = (0,0)
     if (r < d.S) {                                   // init(s), lp.py:69-72
       int s = (int)r, n = d.snode[s];
       for (int j = d.out_ptr[n]; j < d.out_ptr[n + 1]; ++j) em.put(varF(d, s, d.out_e[j], 0), false);
       em.put(varB(d, s, d.gpu_of[n], 0), false);
       rlo = rhi = d.out_units[s];
+      if (d.dict_row) rc = 1 + d.src_ouidx[s];
     } else if (r < d.R_cons) {                       // cap(e,k), lp.py:74-77
       int64_t q = r - d.S;
       int e = (int)(q / K), k = (int)(q % K);
       for (int s = 0; s < d.S; ++s) em.put(varF(d, s, e, k), false);
       rlo = -INFINITY;
       rhi = d.ecap[(int64_t)e * K + k];
+      if (d.dict_row) rc = 1 + d.nOU + d.cap_idx[q];
     } else if (r < d.R_cum) {                        // cons / last, lp.py:81-116
       int64_t q = r - d.R_cons;
       int s = (int)(q / d.CB);
@@ -151,10 +161,12 @@ __global__ void te_rows_kernel(TeDev d, const int64_t* __restrict__ row_ptr,
       for (int s = 0; s < d.S; ++s) em.put(varB(d, s, g, k), false);
       rlo = -INFINITY;
       rhi = d.blimit;
+      rc = 1 + d.nOU + d.nCap;
     }
     if (FILL) {
       lo[r] = rlo;
       hi[r] = rhi;
+      if (d.dict_row) code[r] = (uint16_t)rc;
     } else {
       row_len[r] = em.cnt;
     }
@@ -178,7 +190,7 @@ template <bool FILL>
 __global__ void te_cols_kernel(TeDev d, const int64_t* __restrict__ col_ptr,
                                uint32_t* __restrict__ row, int64_t* __restrict__ col_len,
                                double* __restrict__ lb, double* __restrict__ ub,
-                               double* __restrict__ obj) {
+                               double* __restrict__ obj, uint16_t* __restrict__ code) {
   const int K = d.K;
   const int64_t fB = (int64_t)d.E * K;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < d.n_vars;
@@ -187,6 +199,7 @@ __global__ void te_cols_kernel(TeDev d, const int64_t* __restrict__ col_ptr,
     bool neg[6];
     int c = 0;
     double vlb = 0.0, vub = INFINITY, cost = 0.0;
+    int cc = 0;                                      // bound class 0 = (0, inf, 0)
     if (v < (int64_t)d.S * d.SB) {
       int s = (int)(v / d.SB);
       int64_t q = v % d.SB;
@@ -201,7 +214,7 @@ __global__ void te_cols_kernel(TeDev d, const int64_t* __restrict__ col_ptr,
         if (t == K - 1 && !d.is_sw[w] && w != d.snode[s]) {
           rows[c] = rowCons(d, s, w, K); neg[c++] = false;
         }
-        if (k == 0 && u != d.snode[s]) vub = 0.0;    // lp.py:51-52
+        if (k == 0 && u != d.snode[s]) { vub = 0.0; cc = 1; }   // lp.py:51-52
       } else {                                       // B(s,g,k)
         q -= fB;
         int g = (int)(q / (K + 1)), k = (int)(q % (K + 1));
@@ -210,7 +223,7 @@ __global__ void te_cols_kernel(TeDev d, const int64_t* __restrict__ col_ptr,
         if (k >= 1) { rows[c] = rowCons(d, s, n, k - 1); neg[c++] = true; }
         if (k <= K - 1) { rows[c] = rowCons(d, s, n, k); neg[c++] = false; }
         if (d.has_bcap) { rows[c] = d.R_bcap + (int64_t)g * (K + 1) + k; neg[c++] = false; }
-        if (k == 0 && n != d.snode[s]) vub = 0.0;    // lp.py:57-59
+        if (k == 0 && n != d.snode[s]) { vub = 0.0; cc = 1; }   // lp.py:57-59
       }
     } else {
       int64_t q = v - (int64_t)d.S * d.SB;
@@ -221,6 +234,7 @@ __global__ void te_cols_kernel(TeDev d, const int64_t* __restrict__ col_ptr,
       double u = d.pair_u[p];
       vub = u;
       if (!is_rc) {                                  // Rd(p,k)
+        if (d.dict_col) cc = 2 + d.pair_uidx[p];
         rows[c] = rowCons(d, s, w, k); neg[c++] = true;
         if (k == K - 1) { rows[c] = rowCons(d, s, w, K); neg[c++] = true; }
         rows[c] = d.R_cum + (int64_t)p * K + k; neg[c++] = true;
@@ -229,6 +243,7 @@ __global__ void te_cols_kernel(TeDev d, const int64_t* __restrict__ col_ptr,
         if (k + 1 <= K - 1) { rows[c] = d.R_cum + (int64_t)p * K + k + 1; neg[c++] = true; }
         if (k == K - 1) vlb = u;                     // lp.py:64-65
         cost = -1.0 / (double)(k + 1);               // maximise sum Rc/(k+1), lp.py:133-135
+        if (d.dict_col) cc = 2 + d.nU + d.pair_uidx[p] * K + k;
       }
     }
     if (FILL) {
@@ -238,6 +253,7 @@ __global__ void te_cols_kernel(TeDev d, const int64_t* __restrict__ col_ptr,
       lb[v] = vlb;
       ub[v] = vub;
       obj[v] = cost;
+      if (d.dict_col) code[v] = (uint16_t)cc;
     } else {
       col_len[v] = c;
     }
@@ -403,15 +419,84 @@ extern "C" int teccl_lp_build_te(teccl_ctx* ctx, const teccl_te_desc* desc, tecc
   TECCL_CUDA(cudaMallocAsync((void**)&lp->var_ub, (n + 1) * sizeof(double), st));
   TECCL_CUDA(cudaMallocAsync((void**)&lp->obj, (n + 1) * sizeof(double), st));
 
+  // Bound-class dictionaries (pdlp.cu reads bounds/costs through them).
+  // Columns: [0] free (0,inf,0), [1] fixed (0,0,0), [2+u] Rd (0,U_u,0),
+  // [2+nU+u*K+k] Rc (0 or U_u at k=K-1, U_u, -1/(k+1)). Rows: [0] (0,0),
+  // [1+o] init (OU_o,OU_o), [1+nOU+c] cap (-inf,CAP_c), [1+nOU+nCap] bcap.
+  {
+    std::vector<double> U(desc->pair_units, desc->pair_units + desc->num_pairs);
+    std::sort(U.begin(), U.end());
+    U.erase(std::unique(U.begin(), U.end()), U.end());
+    std::vector<int> puidx(desc->num_pairs);
+    for (int p = 0; p < desc->num_pairs; ++p)
+      puidx[p] = (int)(std::lower_bound(U.begin(), U.end(), desc->pair_units[p]) - U.begin());
+    std::vector<double> ou(desc->num_sources, 0.0);
+    for (int p = 0; p < desc->num_pairs; ++p) ou[desc->pair_source[p]] += desc->pair_units[p];
+    std::vector<double> OU(ou);
+    std::sort(OU.begin(), OU.end());
+    OU.erase(std::unique(OU.begin(), OU.end()), OU.end());
+    std::vector<int> souidx(desc->num_sources);
+    for (int s = 0; s < desc->num_sources; ++s)
+      souidx[s] = (int)(std::lower_bound(OU.begin(), OU.end(), ou[s]) - OU.begin());
+    const size_t EK = (size_t)desc->num_edges * desc->K;
+    std::vector<double> CAPS(desc->edge_cap, desc->edge_cap + EK);
+    std::sort(CAPS.begin(), CAPS.end());
+    CAPS.erase(std::unique(CAPS.begin(), CAPS.end()), CAPS.end());
+    const int K = desc->K, nU = (int)U.size(), nOU = (int)OU.size(), nCap = (int)CAPS.size();
+    const int64_t ncd = 2 + (int64_t)nU * (K + 1);
+    const int64_t nrd = 1 + nOU + nCap + 1;
+    d.nU = nU; d.nOU = nOU; d.nCap = nCap;
+    d.dict_col = ncd <= kMaxDict;
+    d.dict_row = nrd <= kMaxDict;
+    if (d.dict_col) {
+      std::vector<double> cd(3 * ncd);
+      auto put = [&](int64_t i, double a, double b, double c) { cd[3 * i] = a; cd[3 * i + 1] = b; cd[3 * i + 2] = c; };
+      put(0, 0.0, INFINITY, 0.0);
+      put(1, 0.0, 0.0, 0.0);
+      for (int u = 0; u < nU; ++u) put(2 + u, 0.0, U[u], 0.0);
+      for (int u = 0; u < nU; ++u)
+        for (int k = 0; k < K; ++k)
+          put(2 + nU + (int64_t)u * K + k, k == K - 1 ? U[u] : 0.0, U[u], -1.0 / (double)(k + 1));
+      int* dp = nullptr;
+      if (upload(puidx, &dp, st)) return TECCL_ECUDA;
+      owned.push_back(dp);
+      d.pair_uidx = dp;
+      if (upload(cd, &lp->col_dict, st)) return TECCL_ECUDA;
+      lp->n_col_dict = (int32_t)ncd;
+      TECCL_CUDA(cudaMallocAsync((void**)&lp->col_code, (n + 1) * sizeof(uint16_t), st));
+    }
+    if (d.dict_row) {
+      std::vector<double> rd(2 * nrd);
+      rd[0] = 0.0; rd[1] = 0.0;
+      for (int o = 0; o < nOU; ++o) { rd[2 * (1 + o)] = OU[o]; rd[2 * (1 + o) + 1] = OU[o]; }
+      for (int c = 0; c < nCap; ++c) { rd[2 * (1 + nOU + c)] = -INFINITY; rd[2 * (1 + nOU + c) + 1] = CAPS[c]; }
+      rd[2 * (nrd - 1)] = -INFINITY;
+      rd[2 * (nrd - 1) + 1] = desc->buffer_limit;
+      std::vector<uint16_t> cidx(EK);
+      for (size_t q = 0; q < EK; ++q)
+        cidx[q] = (uint16_t)(std::lower_bound(CAPS.begin(), CAPS.end(), desc->edge_cap[q]) - CAPS.begin());
+      int* so = nullptr;
+      uint16_t* ci = nullptr;
+      if (upload(souidx, &so, st) || upload(cidx, &ci, st)) return TECCL_ECUDA;
+      owned.push_back(so);
+      owned.push_back(ci);
+      d.src_ouidx = so;
+      d.cap_idx = ci;
+      if (upload(rd, &lp->row_dict, st)) return TECCL_ECUDA;
+      lp->n_row_dict = (int32_t)nrd;
+      TECCL_CUDA(cudaMallocAsync((void**)&lp->row_code, (m + 1) * sizeof(uint16_t), st));
+    }
+  }
+
   if (m > 0) {
-    te_rows_kernel<false><<<grid_for(m), kThreads, 0, st>>>(d, nullptr, nullptr, row_len, nullptr, nullptr);
+    te_rows_kernel<false><<<grid_for(m), kThreads, 0, st>>>(d, nullptr, nullptr, row_len, nullptr, nullptr, nullptr);
     TECCL_CHECK_LAUNCH();
     if (scan_lengths(row_len, lp->row_ptr, m, st)) return TECCL_ECUDA;
   } else {
     TECCL_CUDA(cudaMemsetAsync(lp->row_ptr, 0, sizeof(int64_t), st));
   }
   if (n > 0) {
-    te_cols_kernel<false><<<grid_for(n), kThreads, 0, st>>>(d, nullptr, nullptr, col_len, nullptr, nullptr, nullptr);
+    te_cols_kernel<false><<<grid_for(n), kThreads, 0, st>>>(d, nullptr, nullptr, col_len, nullptr, nullptr, nullptr, nullptr);
     TECCL_CHECK_LAUNCH();
     if (scan_lengths(col_len, lp->col_ptr, n, st)) return TECCL_ECUDA;
   } else {
@@ -429,11 +514,11 @@ extern "C" int teccl_lp_build_te(teccl_ctx* ctx, const teccl_te_desc* desc, tecc
   TECCL_CUDA(cudaMallocAsync((void**)&lp->col, (nnz_r + 1) * sizeof(uint32_t), st));
   TECCL_CUDA(cudaMallocAsync((void**)&lp->row, (nnz_r + 1) * sizeof(uint32_t), st));
   if (m > 0) {
-    te_rows_kernel<true><<<grid_for(m), kThreads, 0, st>>>(d, lp->row_ptr, lp->col, nullptr, lp->row_lo, lp->row_hi);
+    te_rows_kernel<true><<<grid_for(m), kThreads, 0, st>>>(d, lp->row_ptr, lp->col, nullptr, lp->row_lo, lp->row_hi, lp->row_code);
     TECCL_CHECK_LAUNCH();
   }
   if (n > 0) {
-    te_cols_kernel<true><<<grid_for(n), kThreads, 0, st>>>(d, lp->col_ptr, lp->row, nullptr, lp->var_lb, lp->var_ub, lp->obj);
+    te_cols_kernel<true><<<grid_for(n), kThreads, 0, st>>>(d, lp->col_ptr, lp->row, nullptr, lp->var_lb, lp->var_ub, lp->obj, lp->col_code);
     TECCL_CHECK_LAUNCH();
   }
   TECCL_CUDA(cudaFreeAsync(row_len, st));

@@ -40,6 +40,7 @@ class SolverOptions:
     max_iters: int = 2_000_000
     check_every: int = 64
     device: int = 0
+    pdlp: dict = field(default_factory=dict)   # raw teccl_pdlp_opts overrides (tuning)
 
     def __post_init__(self):
         if not (0 <= self.relative_gap < 1):
@@ -78,6 +79,8 @@ def pdlp_options(opts: SolverOptions, verbose: int = 0) -> nat.PdlpOpts:
     o.time_limit = float(opts.time_limit)
     o.check_every = int(opts.check_every)
     o.verbose = int(verbose)
+    for k, v in opts.pdlp.items():
+        setattr(o, k, type(getattr(o, k))(v))
     return o
 
 
