@@ -40,6 +40,12 @@ extern "C" int teccl_ctx_create(int device, teccl_ctx** out) {
     return TECCL_ENODEV;
   }
   TECCL_CUDA(cudaSetDevice(device));
+  // keep freed stream-ordered allocations in the pool instead of returning
+  // them to the driver at every synchronisation (solves allocate ~100 MB)
+  cudaMemPool_t pool;
+  TECCL_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+  uint64_t keep = UINT64_MAX;
+  TECCL_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
   teccl_ctx* c = new teccl_ctx();
   c->device = device;
   c->sm_count = prop.multiProcessorCount;
@@ -274,6 +280,7 @@ extern "C" int teccl_lp_destroy(teccl_lp* lp) {
   if (!lp) return TECCL_OK;
   cudaSetDevice(lp->device);
   cudaDeviceSynchronize();
+  if (lp->pdlp_ws && lp->ws_free) lp->ws_free(lp->pdlp_ws);
   void* ptrs[] = {lp->row_ptr, lp->col, lp->val, lp->col_ptr, lp->row, lp->cval,
                   lp->row_lo, lp->row_hi, lp->var_lb, lp->var_ub, lp->obj,
                   lp->srow_off, lp->srow_w, lp->srow_idx, lp->srow_val,

@@ -87,6 +87,10 @@ struct teccl_lp {
   double* col_dict = nullptr;      // [3 * n_col_dict]
   double* row_dict = nullptr;      // [2 * n_row_dict]
   int32_t n_col_dict = 0, n_row_dict = 0;
+  // PDLP workspace kept across solves of this LP (buffers, chunk graph,
+  // pinned state ring); freed by teccl_lp_destroy through ws_free
+  void* pdlp_ws = nullptr;
+  void (*ws_free)(void*) = nullptr;
 };
 
 constexpr int kMaxDict = 65536;

@@ -33,6 +33,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -542,21 +543,44 @@ __global__ void hash_fill_kernel(int64_t count, double* v) {
 // ---------------------------------------------------------------------------
 // Host orchestration.
 
+// Solver workspace, created on the first solve of an LP and reused by every
+// later solve of it: device buffers, the captured chunk graph (its kernel
+// arguments point into these buffers) and the pinned state ring.
 struct Workspace {
   std::vector<void*> bufs;
-  cudaStream_t st;
+  int device = 0;
+  double *R = nullptr, *C = nullptr, *rstat = nullptr, *cstat = nullptr;
+  float *D = nullptr, *E = nullptr, *x0 = nullptr, *y0 = nullptr;
+  double *x = nullptr, *xt = nullptr, *xbar = nullptr, *y = nullptr, *yt = nullptr;
+  double *part = nullptr, *part2 = nullptr;
+  PdlpState* dst = nullptr;
+  int64_t pstride = 0;
+  cudaGraphExec_t gexec = nullptr;
+  int graph_chunk = 0;
+  PdlpState* ring = nullptr;
+  int ring_len = 0;
+  std::vector<cudaEvent_t> evs;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   ~Workspace() {
-    for (void* p : bufs) cudaFreeAsync(p, st);
+    cudaSetDevice(device);
+    cudaDeviceSynchronize();
+    for (void* p : bufs) cudaFree(p);
+    if (gexec) cudaGraphExecDestroy(gexec);
+    if (ring) cudaFreeHost(ring);
+    for (auto e : evs) cudaEventDestroy(e);
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
   }
   template <typename T>
   T* alloc(int64_t count) {
     void* p = nullptr;
-    if (cudaMallocAsync(&p, (size_t)(count > 0 ? count : 1) * sizeof(T), st) != cudaSuccess)
-      return nullptr;
+    if (cudaMalloc(&p, (size_t)(count > 0 ? count : 1) * sizeof(T)) != cudaSuccess) return nullptr;
     bufs.push_back(p);
     return (T*)p;
   }
 };
+
+void free_workspace(void* w) { delete (Workspace*)w; }
 
 int read_partials(double* dpart, int count, cudaStream_t st, double* out) {
   std::vector<double> h(count);
@@ -612,30 +636,50 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
                double* y_dev, teccl_pdlp_result* res, StepBench* sb) {
   cudaStream_t st = ctx->stream;
   const int32_t m = lp->m, n = lp->n;
-  Workspace W;
-  W.st = st;
-  cudaEvent_t ev0, ev1;
-  TECCL_CUDA(cudaEventCreate(&ev0));
-  TECCL_CUDA(cudaEventCreate(&ev1));
+  const int nb_row = (int)((m + kTile - 1) / kTile), nb_col = (int)((n + kTile - 1) / kTile);
+  Workspace* ws = (Workspace*)lp->pdlp_ws;
+  if (!ws) {
+    ws = new Workspace();
+    ws->device = ctx->device;
+    Workspace& W = *ws;
+    W.pstride = std::max<int64_t>(std::max(nb_row, nb_col), kGrid);
+    W.R = W.alloc<double>(m + 1); W.C = W.alloc<double>(n + 1);
+    W.rstat = W.alloc<double>(m); W.cstat = W.alloc<double>(n);
+    W.D = W.alloc<float>(n); W.E = W.alloc<float>(m);
+    W.x0 = W.alloc<float>(n); W.y0 = W.alloc<float>(m);
+    W.x = W.alloc<double>(n); W.xt = W.alloc<double>(n + 1); W.xbar = W.alloc<double>(n + 1);
+    W.y = W.alloc<double>(m + 1); W.yt = W.alloc<double>(m + 1);
+    W.part = W.alloc<double>((int64_t)kNQ * W.pstride);
+    W.part2 = W.alloc<double>(kGrid);
+    W.dst = W.alloc<PdlpState>(1);
+    const bool ok = W.R && W.C && W.rstat && W.cstat && W.D && W.E && W.x0 && W.y0 && W.x &&
+                    W.xt && W.xbar && W.y && W.yt && W.part && W.part2 && W.dst;
+    if (!ok || cudaEventCreate(&W.ev0) != cudaSuccess || cudaEventCreate(&W.ev1) != cudaSuccess) {
+      delete ws;
+      set_error("device allocation failed for PDLP workspace");
+      return TECCL_ENOMEM;
+    }
+    lp->pdlp_ws = ws;
+    lp->ws_free = free_workspace;
+  }
+  Workspace& W = *ws;
+  cudaEvent_t ev0 = W.ev0, ev1 = W.ev1;
   TECCL_CUDA(cudaEventRecord(ev0, st));
   auto t_start = std::chrono::steady_clock::now();
-
-  const int nb_row = (int)((m + kTile - 1) / kTile), nb_col = (int)((n + kTile - 1) / kTile);
-  const int64_t pstride = std::max<int64_t>(std::max(nb_row, nb_col), kGrid);
-  double *R = W.alloc<double>(m + 1), *C = W.alloc<double>(n + 1), *rstat = W.alloc<double>(m),
-         *cstat = W.alloc<double>(n);
-  float *D = W.alloc<float>(n), *E = W.alloc<float>(m);
-  float *x0 = W.alloc<float>(n), *y0 = W.alloc<float>(m);
-  double *x = W.alloc<double>(n), *xt = W.alloc<double>(n + 1), *xbar = W.alloc<double>(n + 1);
-  double *y = W.alloc<double>(m + 1), *yt = W.alloc<double>(m + 1);
-  double* part = W.alloc<double>((int64_t)kNQ * pstride);
-  double* part2 = W.alloc<double>(kGrid);
-  PdlpState* dst = W.alloc<PdlpState>(1);
-  if (!R || !C || !rstat || !cstat || !D || !E || !x0 || !y0 || !x || !xt || !xbar || !y || !yt ||
-      !part || !part2 || !dst) {
-    set_error("device allocation failed for PDLP workspace");
-    return TECCL_ENOMEM;
-  }
+  const bool trace = getenv("TECCL_TRACE") != nullptr;
+  auto mark = [&](const char* what) {
+    if (trace) {
+      cudaStreamSynchronize(st);
+      fprintf(stderr, "[teccl trace] %-14s %8.3f ms\n", what,
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count());
+    }
+  };
+  const int64_t pstride = W.pstride;
+  double *R = W.R, *C = W.C, *rstat = W.rstat, *cstat = W.cstat;
+  float *D = W.D, *E = W.E, *x0 = W.x0, *y0 = W.y0;
+  double *x = W.x, *xt = W.xt, *xbar = W.xbar, *y = W.y, *yt = W.yt;
+  double *part = W.part, *part2 = W.part2;
+  PdlpState* dst = W.dst;
   TECCL_CUDA(cudaMemsetAsync(part, 0, sizeof(double) * kNQ * pstride, st));
   // always-zero slots the SELL padding gathers from
   TECCL_CUDA(cudaMemsetAsync(xt, 0, sizeof(double) * (n + 1), st));
@@ -648,6 +692,7 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
   }
   const int gr = grid_for(m > n ? m : n);
   int64_t nl = 0;  // kernel launches issued by this solve
+  mark("setup+sell");
 
   // --- Ruiz equilibration + Pock-Chambolle (alpha = 1), simultaneous updates
   fill_kernel<<<gr, kThreads, 0, st>>>(m, R, 1.0);
@@ -667,6 +712,7 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
   }
   TECCL_CHECK_LAUNCH();
 
+  mark("equilibrate");
   // --- preconditioners (fp32, exact from here on) and their square roots
   double* rootE = rstat;
   double* rootD = cstat;
@@ -718,6 +764,7 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
   }
   TECCL_CHECK_LAUNCH();
 
+  mark("power-iter");
   // --- state: omega in original space = scaled weight * gamma / beta
   PdlpState hs{};
   hs.eta = 0.998 / sigma_max;
@@ -786,26 +833,41 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
     return TECCL_OK;
   }
 
-  // --- chunk graph
-  cudaGraphExec_t gexec = nullptr;
-  if (o->use_graphs) {
+  // --- chunk graph (captured once per LP and chunk length)
+  if (o->use_graphs && W.gexec && W.graph_chunk != chunk) {
+    cudaGraphExecDestroy(W.gexec);
+    W.gexec = nullptr;
+  }
+  if (o->use_graphs && !W.gexec) {
     cudaGraph_t g;
     cudaStream_t cap;
     TECCL_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
     TECCL_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
     enqueue_chunk<UNIT, DICT>(chunk, cap, lp, V);
     TECCL_CUDA(cudaStreamEndCapture(cap, &g));
-    TECCL_CUDA(cudaGraphInstantiate(&gexec, g, 0));
+    TECCL_CUDA(cudaGraphInstantiate(&W.gexec, g, 0));
     TECCL_CUDA(cudaGraphDestroy(g));
     TECCL_CUDA(cudaStreamDestroy(cap));
+    W.graph_chunk = chunk;
   }
+  cudaGraphExec_t gexec = o->use_graphs ? W.gexec : nullptr;
 
+  mark("graph");
   // --- iterate: chunks queued `lookahead` deep; the device stops itself
   const int look = o->lookahead > 0 ? o->lookahead : 1;
-  PdlpState* ring = nullptr;
-  TECCL_CUDA(cudaMallocHost((void**)&ring, sizeof(PdlpState) * look));
-  std::vector<cudaEvent_t> evs(look);
-  for (auto& e : evs) TECCL_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  if (W.ring_len < look) {
+    if (W.ring) cudaFreeHost(W.ring);
+    W.ring = nullptr;
+    TECCL_CUDA(cudaMallocHost((void**)&W.ring, sizeof(PdlpState) * look));
+    W.ring_len = look;
+  }
+  while ((int)W.evs.size() < look) {
+    cudaEvent_t e;
+    TECCL_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    W.evs.push_back(e);
+  }
+  PdlpState* ring = W.ring;
+  std::vector<cudaEvent_t>& evs = W.evs;
   int64_t launched = 0, polled = 0;
   int status = TECCL_ITER_LIMIT;
   PdlpState last = hs;
@@ -851,6 +913,7 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
   if (last.done == 1) status = TECCL_OPTIMAL;
   if (last.done == 3) last.done = 0;
 
+  mark("iterate");
   output_kernel<<<gr, kThreads, 0, st>>>(n, m, V, x_dev, y_dev);
   nl += 1;
   TECCL_CHECK_LAUNCH();
@@ -858,12 +921,8 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
   TECCL_CUDA(cudaEventSynchronize(ev1));
   float ms = 0.f;
   TECCL_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
-  for (auto& e : evs) cudaEventDestroy(e);
-  cudaFreeHost(ring);
-  if (gexec) cudaGraphExecDestroy(gexec);
-  cudaEventDestroy(ev0);
-  cudaEventDestroy(ev1);
 
+  mark("teardown");
   res->status = status;
   res->restarts = last.restarts;
   res->iters = last.total;

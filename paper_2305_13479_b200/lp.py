@@ -243,7 +243,7 @@ class DeviceLP:
         out = (C.c_double * 6)()
         nat.check(self.ctx.lib.teccl_pdlp_step_bench(self.ctx.handle, self.handle, int(reps), out))
         return {"ms_col": out[0], "ms_row": out[1], "bytes_col": out[2], "bytes_row": out[3],
-                "gs_col": int(out[4]), "gs_row": int(out[5])}
+                "dict": bool(out[4]), "slice": int(out[5])}
 
     def close(self) -> None:
         if self.handle:

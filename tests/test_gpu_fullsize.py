@@ -1,0 +1,54 @@
+"""Full-size parity on the benchmark LPs (configs[1] and its 1-chunk variant)
+against the reference's own optimum (tests/golden/full_size.json, produced by
+make_golden_full.py from collsched's model + HiGHS)."""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from paper_2305_13479_b200 import (EpochConfig, SolverOptions, check_lp_schedule, epoch_duration,
+                                   generate_demand, lp_completion_epoch, make_plan, solve)
+from paper_2305_13479_b200.lp import build_from_plan
+from paper_2305_13479_b200.topology import ndv2
+
+pytestmark = pytest.mark.gpu
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "full_size.json")))
+
+
+def _plan(ch, K):
+    t = ndv2(2)
+    d = generate_demand("allgather", t, ch, 25000)
+    tau = epoch_duration(t, d.chunk_size, "fastest", 1)
+    return make_plan(t, d, EpochConfig(tau, K, "fastest", 1, d.chunk_size))
+
+
+@pytest.mark.parametrize("name", sorted(GOLD))
+def test_fullsize_objective_residuals_finish_time(name):
+    g = GOLD[name]
+    plan = _plan(g["chunks"], g["K"])
+    lp = build_from_plan(plan)
+    assert (lp.num_vars, lp.num_rows) == (g["num_vars"], g["num_rows"])
+    # north_star: objective within 1e-4 relative, residuals within 1e-6 relative;
+    # solved to 1e-8 so the finish time and the integer replay are exact-ish
+    sol = solve(lp, SolverOptions(eps_rel=1e-8, time_limit=120))
+    assert sol.status == "optimal"
+    assert sol.meta["rel_primal_res"] <= 1e-6 and sol.meta["rel_dual_res"] <= 1e-6
+    assert sol.objective == pytest.approx(g["objective"], rel=1e-4)
+    assert lp_completion_epoch(sol, tol=1e-5) == g["completion_epoch"]
+    rep = check_lp_schedule(plan, sol.x, tol=1e-5)
+    assert rep.ok, rep
+    assert rep.completion_epoch == g["completion_epoch"]
+
+
+def test_fullsize_time_to_1e4_and_determinism():
+    g = GOLD["ndv2x2_ag2_K530"]
+    lp = build_from_plan(_plan(g["chunks"], g["K"]))
+    a = solve(lp, SolverOptions(eps_rel=1e-4))
+    b = solve(lp, SolverOptions(eps_rel=1e-4))
+    assert a.status == b.status == "optimal"
+    assert a.meta["iters"] == b.meta["iters"]
+    assert np.array_equal(a.x, b.x)
+    assert a.meta["rel_gap"] <= 1e-4
+    assert a.objective == pytest.approx(g["objective"], rel=5e-4)
