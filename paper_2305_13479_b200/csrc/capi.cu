@@ -150,6 +150,7 @@ extern "C" int teccl_lp_from_csr(teccl_ctx* ctx, int32_t m, int32_t n, int64_t n
   lp->nnz = nz;
   lp->unit = unit;
   lp->device = ctx->device;
+  lp->stream = st;
   int rc = 0;
   rc |= to_dev(rp, &lp->row_ptr, st);
   rc |= to_dev(ci, &lp->col, st);
@@ -287,7 +288,11 @@ extern "C" int teccl_lp_destroy(teccl_lp* lp) {
                   lp->scol_off, lp->scol_w, lp->scol_idx, lp->scol_val,
                   lp->col_code, lp->row_code, lp->col_dict, lp->row_dict};
   for (void* p : ptrs)
-    if (p) cudaFree(p);
+    if (p) {
+      if (lp->stream) cudaFreeAsync(p, lp->stream);
+      else cudaFree(p);
+    }
+  if (lp->stream) cudaStreamSynchronize(lp->stream);
   delete lp;
   return TECCL_OK;
 }

@@ -69,6 +69,7 @@ struct teccl_lp {
   double* var_ub = nullptr;        // [n]
   double* obj = nullptr;           // [n] minimisation costs
   int device = 0;
+  cudaStream_t stream = nullptr;   // stream the LP's arrays were allocated on
   // SELL-32 copies used by the PDLP iteration kernels (built on first solve)
   bool sell_ready = false;
   int64_t* srow_off = nullptr;

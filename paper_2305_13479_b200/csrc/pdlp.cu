@@ -468,6 +468,25 @@ __global__ void sumsq_kernel(int64_t count, const double* v, double* part) {
   if (threadIdx.x == 0) part[blockIdx.x] = a;
 }
 
+// scal[0] = sum of partials (fixed order), scal[1] = 1/sqrt(scal[0])
+__global__ void __launch_bounds__(1024) finalize_norm_kernel(const double* part, int nb, double* scal) {
+  __shared__ double sh[32];
+  double a = 0.0;
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) a += part[b];
+  a = block_sum(a, sh);
+  if (threadIdx.x == 0) {
+    scal[0] = a;
+    scal[1] = a > 0.0 ? 1.0 / sqrt(a) : 0.0;
+  }
+}
+
+__global__ void scale_by_kernel(int64_t count, double* v, const double* scal) {
+  const double s = scal[1];
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < count;
+       r += (int64_t)gridDim.x * blockDim.x)
+    v[r] *= s;
+}
+
 __global__ void scale_inplace_kernel(int64_t count, double* v, double s) {
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < count;
        r += (int64_t)gridDim.x * blockDim.x)
@@ -549,6 +568,7 @@ __global__ void hash_fill_kernel(int64_t count, double* v) {
 struct Workspace {
   std::vector<void*> bufs;
   int device = 0;
+  cudaStream_t st = nullptr;      // allocations come from the stream-ordered pool
   double *R = nullptr, *C = nullptr, *rstat = nullptr, *cstat = nullptr;
   float *D = nullptr, *E = nullptr, *x0 = nullptr, *y0 = nullptr;
   double *x = nullptr, *xt = nullptr, *xbar = nullptr, *y = nullptr, *yt = nullptr;
@@ -564,7 +584,8 @@ struct Workspace {
   ~Workspace() {
     cudaSetDevice(device);
     cudaDeviceSynchronize();
-    for (void* p : bufs) cudaFree(p);
+    for (void* p : bufs) cudaFreeAsync(p, st);
+    cudaStreamSynchronize(st);
     if (gexec) cudaGraphExecDestroy(gexec);
     if (ring) cudaFreeHost(ring);
     for (auto e : evs) cudaEventDestroy(e);
@@ -574,7 +595,8 @@ struct Workspace {
   template <typename T>
   T* alloc(int64_t count) {
     void* p = nullptr;
-    if (cudaMalloc(&p, (size_t)(count > 0 ? count : 1) * sizeof(T)) != cudaSuccess) return nullptr;
+    if (cudaMallocAsync(&p, (size_t)(count > 0 ? count : 1) * sizeof(T), st) != cudaSuccess)
+      return nullptr;
     bufs.push_back(p);
     return (T*)p;
   }
@@ -641,6 +663,7 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
   if (!ws) {
     ws = new Workspace();
     ws->device = ctx->device;
+    ws->st = st;
     Workspace& W = *ws;
     W.pstride = std::max<int64_t>(std::max(nb_row, nb_col), kGrid);
     W.R = W.alloc<double>(m + 1); W.C = W.alloc<double>(n + 1);
@@ -737,26 +760,33 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
   // A D^1/2 v in yt, E A D^1/2 v in y)
   double sigma_max = 1.0;
   if (m > 0 && n > 0 && lp->nnz > 0) {
+    // 40 rounds fully on the device (norms reduced and applied by kernels);
+    // one host read at the end
+    double* scal = part2;  // part2[0..1]: squared norm, inverse norm
     hash_fill_kernel<<<gr, kThreads, 0, st>>>(n, xt);
-    double nv = 0.0;
     sumsq_kernel<<<kGrid, kThreads, 0, st>>>(n, xt, part);
-    if (read_partials(part, kGrid, st, &nv)) return TECCL_ECUDA;
-    scale_inplace_kernel<<<gr, kThreads, 0, st>>>(n, xt, 1.0 / sqrt(nv));
-    nl += 3;
-    for (int it = 0; it < 40; ++it) {
+    finalize_norm_kernel<<<1, 1024, 0, st>>>(part, kGrid, scal);
+    scale_by_kernel<<<gr, kThreads, 0, st>>>(n, xt, scal);
+    nl += 4;
+    const int rounds = 40;
+    for (int it = 0; it < rounds; ++it) {
       mul_kernel<<<gr, kThreads, 0, st>>>(n, xbar, xt, rootD);
       spmv_scaled_kernel<UNIT><<<gr, kThreads, 0, st>>>(m, lp->row_ptr, lp->col, lp->val, xbar, nullptr, yt);
       mul_kernel<<<gr, kThreads, 0, st>>>(m, y, yt, rootE);
       mul_kernel<<<gr, kThreads, 0, st>>>(m, y, y, rootE);
       spmv_scaled_kernel<UNIT><<<gr, kThreads, 0, st>>>(n, lp->col_ptr, lp->row, lp->cval, y, rootD, xt);
       sumsq_kernel<<<kGrid, kThreads, 0, st>>>(n, xt, part);
-      nl += 6;
-      if (read_partials(part, kGrid, st, &nv)) return TECCL_ECUDA;
-      if (!(nv > 0.0)) break;
-      scale_inplace_kernel<<<gr, kThreads, 0, st>>>(n, xt, 1.0 / sqrt(nv));
-      nl += 1;
+      finalize_norm_kernel<<<1, 1024, 0, st>>>(part, kGrid, scal);
+      nl += 7;
+      if (it + 1 < rounds) {
+        scale_by_kernel<<<gr, kThreads, 0, st>>>(n, xt, scal);
+        nl += 1;
+      }
     }
-    if (nv > 0.0) sigma_max = sqrt(sqrt(nv));
+    double nv = 0.0;
+    TECCL_CUDA(cudaMemcpyAsync(&nv, scal, sizeof(double), cudaMemcpyDeviceToHost, st));
+    TECCL_CUDA(cudaStreamSynchronize(st));
+    if (nv > 0.0 && std::isfinite(nv)) sigma_max = sqrt(sqrt(nv));
     TECCL_CUDA(cudaMemsetAsync(xbar, 0, sizeof(double) * (n + 1), st));
     TECCL_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * (m + 1), st));
     TECCL_CUDA(cudaMemsetAsync(xt, 0, sizeof(double) * (n + 1), st));

@@ -407,6 +407,7 @@ extern "C" int teccl_lp_build_te(teccl_ctx* ctx, const teccl_te_desc* desc, tecc
   lp->n = (int32_t)d.n_vars;
   lp->unit = true;
   lp->device = ctx->device;
+  lp->stream = st;
   const int64_t m = d.n_rows, n = d.n_vars;
   int64_t *row_len = nullptr, *col_len = nullptr;
   TECCL_CUDA(cudaMallocAsync((void**)&lp->row_ptr, (m + 1) * sizeof(int64_t), st));
