@@ -40,6 +40,7 @@ extern "C" {
 #define TECCL_TIME_LIMIT 2     /* time_limit reached */
 #define TECCL_PRIMAL_INFEASIBLE 3
 #define TECCL_NUMERICAL 4
+#define TECCL_PEER_TIMEOUT 5    /* a peer rank stopped answering (row-partitioned solve) */
 
 typedef struct teccl_ctx teccl_ctx; /* one device + one stream */
 typedef struct teccl_lp teccl_lp;   /* device-resident LP: CSR, CSC, bounds, costs */
@@ -78,6 +79,24 @@ typedef struct {
 } teccl_te_desc;
 
 int teccl_lp_build_te(teccl_ctx* ctx, const teccl_te_desc* desc, teccl_lp** out);
+
+/* Row-partitioned build (north_star: a single LP row-partitioned by epoch
+ * block over GPUs). Rank `rank` of `world` builds only its epoch block of the
+ * LP in epoch-major numbering: owned rows and
+ * columns plus the halo windows its SpMVs gather from. info[16] receives
+ * {own_c0, own_c1, own_r0, own_r1, win_c0, win_c1, win_r0, win_r1, k0, k1,
+ *  total_cols, total_rows, delta_max, nnz_csr, nnz_csc, cols_per_epoch}. */
+int teccl_lp_build_te_part(teccl_ctx* ctx, const teccl_te_desc* desc, int32_t world,
+                           int32_t rank, teccl_lp** out, int64_t* info);
+
+/* Peer exchange for a row-partitioned LP (one process per GPU). Each rank
+ * exports a blob (CUDA IPC handle of its exchange arena + layout, *blob_len
+ * bytes, <= 512), the host all-gathers the blobs in rank order and every
+ * rank connects to all of them; teccl_pdlp_solve then runs the partitioned
+ * solve on all ranks together, halo vectors and KKT scalars moving through
+ * peer memory over NVLink. */
+int teccl_dist_export(teccl_ctx* ctx, teccl_lp* lp, uint8_t* blob, int64_t* blob_len);
+int teccl_dist_connect(teccl_ctx* ctx, teccl_lp* lp, const uint8_t* blobs, int64_t blob_len);
 
 /* Generic LP upload (minimise obj.x s.t. row_lo <= A x <= row_hi,
  * var_lb <= x <= var_ub; +-INFINITY allowed). Replaces the matrix assembly of

@@ -18,14 +18,15 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 # Every symbol include/teccl_b200.h declares (tests check the export table).
 EXPORTED = (
     "teccl_last_error", "teccl_version", "teccl_ctx_create", "teccl_ctx_destroy",
-    "teccl_ctx_sync", "teccl_lp_build_te", "teccl_lp_from_csr", "teccl_lp_dims",
+    "teccl_ctx_sync", "teccl_lp_build_te", "teccl_lp_build_te_part", "teccl_dist_export",
+    "teccl_dist_connect", "teccl_lp_from_csr", "teccl_lp_dims",
     "teccl_lp_export", "teccl_lp_export_csc", "teccl_lp_destroy",
     "teccl_pdlp_default_opts", "teccl_pdlp_solve", "teccl_pdlp_solve_dev",
     "teccl_spmv_bench", "teccl_pdlp_step_bench", "teccl_check_te", "teccl_check_te_dev",
 )
 
 STATUS = {0: "optimal", 1: "iteration-limit", 2: "time-limit", 3: "primal-infeasible",
-          4: "numerical"}
+          4: "numerical", 5: "peer-timeout"}
 
 _p = C.POINTER
 
@@ -98,6 +99,10 @@ def load(path: str | None = None):
             "teccl_ctx_destroy": (C.c_int, [vp]),
             "teccl_ctx_sync": (C.c_int, [vp]),
             "teccl_lp_build_te": (C.c_int, [vp, _p(TeDesc), _p(vp)]),
+            "teccl_lp_build_te_part": (C.c_int, [vp, _p(TeDesc), C.c_int32, C.c_int32, _p(vp),
+                                                 _p(C.c_int64)]),
+            "teccl_dist_export": (C.c_int, [vp, vp, _p(C.c_uint8), _p(C.c_int64)]),
+            "teccl_dist_connect": (C.c_int, [vp, vp, _p(C.c_uint8), C.c_int64]),
             "teccl_lp_from_csr": (C.c_int, [vp, C.c_int32, C.c_int32, C.c_int64, _p(C.c_int64),
                                             _p(C.c_int32), _p(C.c_double), _p(C.c_double),
                                             _p(C.c_double), _p(C.c_double), _p(C.c_double),

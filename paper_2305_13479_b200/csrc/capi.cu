@@ -234,20 +234,21 @@ int export_matrix(const teccl_lp* lp, bool csc, int64_t* ptr, int32_t* idx, doub
   const int64_t* dptr = csc ? lp->col_ptr : lp->row_ptr;
   const uint32_t* didx = csc ? lp->row : lp->col;
   const double* dval = csc ? lp->cval : lp->val;
+  const int64_t nz = (csc && lp->nnz_csc >= 0) ? lp->nnz_csc : lp->nnz;
   if (ptr) TECCL_CUDA(cudaMemcpy(ptr, dptr, (major + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost));
   if (idx || val) {
-    std::vector<uint32_t> raw(lp->nnz);
-    if (lp->nnz) TECCL_CUDA(cudaMemcpy(raw.data(), didx, lp->nnz * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    std::vector<uint32_t> raw(nz);
+    if (nz) TECCL_CUDA(cudaMemcpy(raw.data(), didx, nz * sizeof(uint32_t), cudaMemcpyDeviceToHost));
     if (lp->unit) {
-      for (int64_t p = 0; p < lp->nnz; ++p) {
+      for (int64_t p = 0; p < nz; ++p) {
         if (idx) idx[p] = (int32_t)(raw[p] & kIdxMask);
         if (val) val[p] = (raw[p] & kSignBit) ? -1.0 : 1.0;
       }
     } else {
-      for (int64_t p = 0; p < lp->nnz; ++p)
+      for (int64_t p = 0; p < nz; ++p)
         if (idx) idx[p] = (int32_t)raw[p];
-      if (val && lp->nnz)
-        TECCL_CUDA(cudaMemcpy(val, dval, lp->nnz * sizeof(double), cudaMemcpyDeviceToHost));
+      if (val && nz)
+        TECCL_CUDA(cudaMemcpy(val, dval, nz * sizeof(double), cudaMemcpyDeviceToHost));
     }
   }
   return TECCL_OK;
@@ -282,6 +283,7 @@ extern "C" int teccl_lp_destroy(teccl_lp* lp) {
   cudaSetDevice(lp->device);
   cudaDeviceSynchronize();
   if (lp->pdlp_ws && lp->ws_free) lp->ws_free(lp->pdlp_ws);
+  if (lp->dist && lp->dist_free) lp->dist_free(lp->dist);
   void* ptrs[] = {lp->row_ptr, lp->col, lp->val, lp->col_ptr, lp->row, lp->cval,
                   lp->row_lo, lp->row_hi, lp->var_lb, lp->var_ub, lp->obj,
                   lp->srow_off, lp->srow_w, lp->srow_idx, lp->srow_val,

@@ -92,7 +92,25 @@ struct teccl_lp {
   // pinned state ring); freed by teccl_lp_destroy through ws_free
   void* pdlp_ws = nullptr;
   void (*ws_free)(void*) = nullptr;
+  // Row-partitioned (epoch-block) LPs built by teccl_lp_build_te_part: this
+  // device owns global epoch-major rows [own_r0, own_r1) and columns
+  // [own_c0, own_c1); its matrices index the gather windows [win_c0, win_c1)
+  // (columns) and [win_r0, win_r1) (rows). Single-device LPs: part_world = 1.
+  int part_world = 1, part_rank = 0;
+  int64_t em_ncols = 0, em_nrows = 0;
+  int64_t own_c0 = 0, own_c1 = 0, own_r0 = 0, own_r1 = 0;
+  int64_t win_c0 = 0, win_c1 = 0, win_r0 = 0, win_r1 = 0;
+  int64_t nnz_csc = -1;            // CSC entries when they differ from nnz
+  void* dist = nullptr;            // peer-memory exchange state (pdlp.cu)
+  void (*dist_free)(void*) = nullptr;
 };
+
+// lengths of the vectors the SpMVs gather from, and where the owned part
+// starts inside them
+inline int64_t gather_cols(const teccl_lp* lp) { return lp->part_world > 1 ? lp->win_c1 - lp->win_c0 : lp->n; }
+inline int64_t gather_rows(const teccl_lp* lp) { return lp->part_world > 1 ? lp->win_r1 - lp->win_r0 : lp->m; }
+inline int64_t own_col_off(const teccl_lp* lp) { return lp->part_world > 1 ? lp->own_c0 - lp->win_c0 : 0; }
+inline int64_t own_row_off(const teccl_lp* lp) { return lp->part_world > 1 ? lp->own_r0 - lp->win_r0 : 0; }
 
 constexpr int kMaxDict = 65536;
 

@@ -30,10 +30,12 @@
 // kernels. Chunks are replayed from a CUDA graph, queued ahead of the host.
 
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "common.cuh"
@@ -81,7 +83,149 @@ struct Vecs {
   int64_t pstride;
   int nb_row, nb_col;
   PdlpState* st;
+  double* slots;         // [world][kSlots]: every rank's reduced partials
+  int world, rank;
 };
+
+__device__ __forceinline__ double block_sum(double v, double* sh);
+
+constexpr int kSlots = 16;  // doubles per rank in the slot table
+constexpr int kMaxPeers = 8;
+
+// ---------------------------------------------------------------------------
+// Peer-memory exchange for row-partitioned solves (one process per GPU,
+// buffers shared through CUDA IPC over NVLink/NVSwitch). A "halo event"
+// copies this rank's owned boundary entries straight into the neighbours'
+// window arrays and then publishes a sequence number into their flag
+// arrays; a wait kernel spins (acquire, system scope, with a timeout) until
+// the neighbours' sequence numbers for the same event have arrived. Every
+// rank issues the same sequence of events, so sequence numbers line up.
+struct Signal {
+  unsigned long long* peer_flag[kMaxPeers];  // peer's flags[my rank]
+  int npeer;
+  unsigned long long* seq;                   // my event counter
+  unsigned int* arrive;                      // last-block election
+};
+struct Halo {
+  const double* src[2 * kMaxPeers];
+  double* dst[2 * kMaxPeers];
+  int64_t cnt[2 * kMaxPeers];
+  int n;
+};
+struct Wait {
+  const unsigned long long* flags;           // my flags[world]
+  int peer[kMaxPeers];
+  int npeer;
+  const unsigned long long* seq;
+};
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ void signal_peers(const Signal& S) {
+  const unsigned long long s = *S.seq + 1;
+  *S.seq = s;
+  __threadfence_system();
+  for (int q = 0; q < S.npeer; ++q) st_release_sys(S.peer_flag[q], s);
+}
+
+// Copy every (src -> peer dst) range, then the last block to finish signals.
+__global__ void halo_kernel(Halo H, Signal S, const PdlpState* st) {
+  if (st && st->done) return;
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int c = 0; c < H.n; ++c)
+    for (int64_t i = tid; i < H.cnt[c]; i += stride) H.dst[c][i] = H.src[c][i];
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int prev = atomicAdd(S.arrive, 1u);
+    if (prev == gridDim.x - 1) {
+      *S.arrive = 0u;
+      signal_peers(S);
+    }
+  }
+}
+
+// Spin until every listed peer has published this rank's current sequence
+// number. A peer that never arrives (crash, mismatch) trips the ~20 s
+// timeout, which stops the solve with done = 4 instead of hanging the GPU.
+__global__ void wait_kernel(Wait Wt, PdlpState* st) {
+  if (threadIdx.x != 0 || (st && st->done)) return;
+  const unsigned long long want = *Wt.seq;
+  const long long t0 = clock64();
+  for (int q = 0; q < Wt.npeer; ++q) {
+    while (ld_acquire_sys(Wt.flags + Wt.peer[q]) < want) {
+      __nanosleep(64);
+      if (clock64() - t0 > 40000000000LL) {
+        if (st) st->done = 4;
+        return;
+      }
+    }
+  }
+}
+
+// Reduce this rank's partial sums to kNQ values, store them in its slot row
+// of every rank's slot table (own + peers), then signal all peers.
+__global__ void __launch_bounds__(1024) reduce_publish_kernel(Vecs V, Signal S,
+                                                              double* const* peer_slots) {
+  __shared__ double sh[32];
+  __shared__ double q[kNQ];
+  if (V.st->done) return;
+  for (int k = 0; k < kNQ; ++k) {
+    const bool row_q = (k == Q_DY || k == Q_DY0 || k == Q_RP || k == Q_DOBJ_ROW);
+    const int nb = row_q ? V.nb_row : V.nb_col;
+    double a = 0.0;
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) a += V.part[k * V.pstride + b];
+    a = block_sum(a, sh);
+    if (threadIdx.x == 0) q[k] = a;
+  }
+  __syncthreads();
+  if (threadIdx.x < kNQ) {
+    V.slots[V.rank * kSlots + threadIdx.x] = q[threadIdx.x];
+    for (int p = 0; p < S.npeer; ++p) peer_slots[p][V.rank * kSlots + threadIdx.x] = q[threadIdx.x];
+    __threadfence_system();  // this thread's peer stores before the flag
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && S.npeer > 0) signal_peers(S);
+}
+
+// Generic scalar all-reduce helpers for the setup phase: publish `count`
+// values (sum of `nb` partials each, stride `pstride`) into the slot tables,
+// then (after a wait) sum the slot rows of every rank in rank order.
+__global__ void __launch_bounds__(1024) publish_values_kernel(const double* part, int nb,
+                                                              int64_t pstride, int count,
+                                                              double* slots, int rank, Signal S,
+                                                              double* const* peer_slots) {
+  __shared__ double sh[32];
+  for (int k = 0; k < count; ++k) {
+    double a = 0.0;
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) a += part[k * pstride + b];
+    a = block_sum(a, sh);
+    if (threadIdx.x == 0) {
+      slots[rank * kSlots + k] = a;
+      for (int p = 0; p < S.npeer; ++p) peer_slots[p][rank * kSlots + k] = a;
+    }
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0 && S.npeer > 0) signal_peers(S);
+}
+
+// out[k] = sum over ranks of slots[r][k]; out[count + k] = 1/sqrt(out[k])
+__global__ void sum_slots_kernel(const double* slots, int world, int count, double* out) {
+  if (threadIdx.x >= count) return;
+  double a = 0.0;
+  for (int r = 0; r < world; ++r) a += slots[r * kSlots + threadIdx.x];
+  out[threadIdx.x] = a;
+  out[count + threadIdx.x] = a > 0.0 ? 1.0 / sqrt(a) : 0.0;
+}
 
 // ---------------------------------------------------------------------------
 // SELL-32 SpMV (layout built by sell.cu): slice s holds rows 32s..32s+31,
@@ -307,23 +451,18 @@ __global__ void __launch_bounds__(kThreads) kkt_col_kernel(int32_t n, SellView S
   if (threadIdx.x == 0) V.part[Q_DOBJ_COL * V.pstride + blockIdx.x] = a;
 }
 
-// Single block: reduce the partials in a fixed order, evaluate termination,
-// decide restarts and update the primal weight. All of PDLP's control flow.
-__global__ void __launch_bounds__(1024) control_kernel(Vecs V) {
-  __shared__ double sh[32];
-  __shared__ double q[kNQ];
+// Sum every rank's reduced partials in rank order (identical on all ranks, so
+// all ranks take the same decisions), evaluate termination, decide restarts
+// and update the primal weight. All of PDLP's control flow.
+__global__ void control_kernel(Vecs V) {
   PdlpState* st = V.st;
-  if (st->done) return;
+  if (threadIdx.x != 0 || st->done) return;
+  double q[kNQ];
   for (int k = 0; k < kNQ; ++k) {
-    const bool row_q = (k == Q_DY || k == Q_DY0 || k == Q_RP || k == Q_DOBJ_ROW);
-    const int nb = row_q ? V.nb_row : V.nb_col;
     double a = 0.0;
-    for (int b = threadIdx.x; b < nb; b += blockDim.x) a += V.part[k * V.pstride + b];
-    a = block_sum(a, sh);
-    if (threadIdx.x == 0) q[k] = a;
+    for (int r = 0; r < V.world; ++r) a += V.slots[r * kSlots + k];  // rank order: same on all ranks
+    q[k] = a;
   }
-  __syncthreads();
-  if (threadIdx.x != 0) return;
   const double w = st->omega;
   const double r = sqrt(w * q[Q_DX] + q[Q_DY] / w);
   const double pobj = q[Q_POBJ];
@@ -375,13 +514,18 @@ __global__ void restart_x_kernel(int32_t n, Vecs V) {
     V.x0[j] = (float)xt;
   }
 }
-__global__ void restart_y_kernel(int32_t m, Vecs V) {
-  if (V.st->done || !V.st->restart) return;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+// Rows: y <- yt over the whole gather window (ghost entries hold the
+// neighbours' yt, which is their new y), y0 <- yt over the owned rows.
+__global__ void restart_y_kernel(int64_t win, int64_t off, int32_t m, double* __restrict__ y_win,
+                                 const double* __restrict__ yt_win, float* __restrict__ y0,
+                                 const PdlpState* st) {
+  if (st->done || !st->restart) return;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < win;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const double yt = V.yt[i];
-    V.y[i] = yt;
-    V.y0[i] = (float)yt;
+    const double yt = yt_win[i];
+    y_win[i] = yt;
+    const int64_t o = i - off;
+    if (o >= 0 && o < m) y0[o] = (float)yt;
   }
 }
 
@@ -560,6 +704,72 @@ __global__ void hash_fill_kernel(int64_t count, double* v) {
 }
 
 // ---------------------------------------------------------------------------
+// Row-partitioned solves: the peer-memory arena of one rank and its view of
+// the other ranks' arenas (CUDA IPC handles exchanged by the host).
+enum ArrayId { A_XBAR = 0, A_XT, A_CW, A_Y, A_YT, A_RW, A_NARR };
+enum MetaId {
+  M_NCW = 0, M_NRW, M_OFF0,  // M_OFF0 .. M_OFF0+A_NARR-1: array byte offsets
+  M_FLAGS = M_OFF0 + A_NARR, M_SLOTS, M_SEQ, M_ARRIVE,
+  M_OC0, M_OC1, M_OR0, M_OR1, M_WC0, M_WC1, M_WR0, M_WR1, M_RANK, M_WORLD, M_COUNT
+};
+constexpr int kMetaLen = 32;
+constexpr int kBlobLen = (int)sizeof(cudaIpcMemHandle_t) + kMetaLen * 8;
+
+struct DistState {
+  int world = 1, rank = 0, device = 0;
+  bool connected = false;
+  char* arena = nullptr;
+  int64_t meta[kMetaLen] = {0};
+  std::vector<std::array<int64_t, kMetaLen>> peer_meta;
+  std::vector<char*> peer_base;      // nullptr for self
+  double** d_peer_slots = nullptr;   // device array: slot tables of all peers (rank order, self skipped)
+  Signal sig_nbr{}, sig_all{};
+  Wait wait_nbr{}, wait_all{};
+
+  double* arr(int id) const { return (double*)(arena + meta[M_OFF0 + id]); }
+  double* slots() const { return (double*)(arena + meta[M_SLOTS]); }
+  bool is_col(int id) const { return id == A_XBAR || id == A_XT || id == A_CW; }
+  void range(int q, int id, int64_t& o0, int64_t& o1, int64_t& w0, int64_t& w1) const {
+    const int64_t* mt = (q == rank) ? meta : peer_meta[q].data();
+    if (is_col(id)) { o0 = mt[M_OC0]; o1 = mt[M_OC1]; w0 = mt[M_WC0]; w1 = mt[M_WC1]; }
+    else { o0 = mt[M_OR0]; o1 = mt[M_OR1]; w0 = mt[M_WR0]; w1 = mt[M_WR1]; }
+  }
+  Halo halo_plan(std::initializer_list<int> ids) const {
+    Halo H{};
+    for (int id : ids)
+      for (int q : {rank - 1, rank + 1}) {
+        if (q < 0 || q >= world || H.n >= 2 * kMaxPeers) continue;
+        int64_t o0, o1, w0, w1, qo0, qo1, qw0, qw1;
+        range(rank, id, o0, o1, w0, w1);
+        range(q, id, qo0, qo1, qw0, qw1);
+        const int64_t a = std::max(o0, qw0), b = std::min(o1, qw1);
+        if (b <= a) continue;
+        H.src[H.n] = arr(id) + (a - w0);
+        H.dst[H.n] = (double*)(peer_base[q] + peer_meta[q][M_OFF0 + id]) + (a - qw0);
+        H.cnt[H.n] = b - a;
+        ++H.n;
+      }
+    return H;
+  }
+  int64_t halo_max(std::initializer_list<int> ids) const {
+    Halo H = halo_plan(ids);
+    int64_t mx = 1;
+    for (int i = 0; i < H.n; ++i) mx = std::max(mx, H.cnt[i]);
+    return mx;
+  }
+  ~DistState() {
+    cudaSetDevice(device);
+    cudaDeviceSynchronize();
+    for (char* b : peer_base)
+      if (b) cudaIpcCloseMemHandle(b);
+    if (d_peer_slots) cudaFree(d_peer_slots);
+    if (arena) cudaFree(arena);
+  }
+};
+
+void free_dist(void* d) { delete (DistState*)d; }
+
+// ---------------------------------------------------------------------------
 // Host orchestration.
 
 // Solver workspace, created on the first solve of an LP and reused by every
@@ -572,7 +782,7 @@ struct Workspace {
   double *R = nullptr, *C = nullptr, *rstat = nullptr, *cstat = nullptr;
   float *D = nullptr, *E = nullptr, *x0 = nullptr, *y0 = nullptr;
   double *x = nullptr, *xt = nullptr, *xbar = nullptr, *y = nullptr, *yt = nullptr;
-  double *part = nullptr, *part2 = nullptr;
+  double *part = nullptr, *part2 = nullptr, *slots = nullptr;
   PdlpState* dst = nullptr;
   int64_t pstride = 0;
   cudaGraphExec_t gexec = nullptr;
@@ -630,28 +840,74 @@ void launch_row(cudaStream_t st, const teccl_lp* lp, const Vecs& V, int j) {
   row_step_kernel<UNIT, DICT, CHECK><<<V.nb_row, kThreads, 0, st>>>(lp->m, row_view(lp), V, j);
 }
 
-template <bool UNIT, bool DICT>
-void enqueue_chunk(int chunk, cudaStream_t st, const teccl_lp* lp, const Vecs& V) {
-  for (int j = 0; j < chunk; ++j) {
-    if (j == chunk - 1) {
-      launch_col<UNIT, DICT, true>(st, lp, V, j);
-      launch_row<UNIT, DICT, true>(st, lp, V, j);
-    } else {
-      launch_col<UNIT, DICT, false>(st, lp, V, j);
-      launch_row<UNIT, DICT, false>(st, lp, V, j);
-    }
-  }
-  kkt_row_kernel<UNIT><<<V.nb_row, kThreads, 0, st>>>(lp->m, row_view(lp), V);
-  kkt_col_kernel<UNIT><<<V.nb_col, kThreads, 0, st>>>(lp->n, col_view(lp), V);
-  control_kernel<<<1, 1024, 0, st>>>(V);
-  restart_x_kernel<<<grid_for(lp->n), kThreads, 0, st>>>(lp->n, V);
-  restart_y_kernel<<<grid_for(lp->m), kThreads, 0, st>>>(lp->m, V);
-}
-
 struct StepBench {
   int reps;
   double ms_col, ms_row, bytes_col, bytes_row;
 };
+
+// Exchange plumbing of one solve: peer-memory halo/reduction events for a
+// row-partitioned LP, nothing for a single-device one.
+struct Exchange {
+  DistState* ds = nullptr;
+  PdlpState* st = nullptr;
+  int64_t nl = 0;
+  bool active() const { return ds != nullptr && ds->world > 1; }
+  // copy owned boundary ranges of the listed window arrays to the
+  // neighbours, signal them, and wait for theirs
+  void halo(cudaStream_t s, std::initializer_list<int> arrays) {
+    if (!active()) return;
+    Halo H = ds->halo_plan(arrays);
+    halo_kernel<<<std::max(1, std::min(kSMs * 2, (int)((ds->halo_max(arrays) + 255) / 256))), 256, 0, s>>>(
+        H, ds->sig_nbr, st);
+    wait_kernel<<<1, 32, 0, s>>>(ds->wait_nbr, st);
+    nl += 2;
+  }
+  void wait_all(cudaStream_t s) {
+    if (!active()) return;
+    wait_kernel<<<1, 32, 0, s>>>(ds->wait_all, st);
+    nl += 1;
+  }
+};
+
+template <bool UNIT, bool DICT>
+void enqueue_chunk(int chunk, cudaStream_t st, const teccl_lp* lp, const Vecs& Vc, const Vecs& Vr,
+                   Exchange& X, double* y_w, double* yt_w) {
+  const int64_t nrw = gather_rows(lp), orr = own_row_off(lp);
+  for (int j = 0; j < chunk; ++j) {
+    const bool check = (j == chunk - 1);
+    if (check) launch_col<UNIT, DICT, true>(st, lp, Vc, j);
+    else launch_col<UNIT, DICT, false>(st, lp, Vc, j);
+    if (check) X.halo(st, {A_XBAR, A_XT});
+    else X.halo(st, {A_XBAR});
+    if (check) launch_row<UNIT, DICT, true>(st, lp, Vr, j);
+    else launch_row<UNIT, DICT, false>(st, lp, Vr, j);
+    if (check) X.halo(st, {A_Y, A_YT});
+    else X.halo(st, {A_Y});
+  }
+  kkt_row_kernel<UNIT><<<Vr.nb_row, kThreads, 0, st>>>(lp->m, row_view(lp), Vr);
+  kkt_col_kernel<UNIT><<<Vc.nb_col, kThreads, 0, st>>>(lp->n, col_view(lp), Vc);
+  reduce_publish_kernel<<<1, 1024, 0, st>>>(Vc, X.active() ? X.ds->sig_all : Signal{},
+                                            X.active() ? X.ds->d_peer_slots : nullptr);
+  X.wait_all(st);
+  control_kernel<<<1, 32, 0, st>>>(Vc);
+  restart_x_kernel<<<grid_for(lp->n), kThreads, 0, st>>>(lp->n, Vc);
+  restart_y_kernel<<<grid_for(nrw), kThreads, 0, st>>>(nrw, orr, lp->m, y_w, yt_w, Vr.y0, Vr.st);
+}
+
+// setup-phase all-reduce of `count` quantities laid out as part[k*pstride+b]
+// (nb partials each); result sums land in out[0..count), inverse roots in
+// out[count..2count). Host-visible after a stream sync.
+int all_reduce(cudaStream_t st, Exchange& X, double* part, int nb, int64_t pstride, int count,
+               double* slots, int world, int rank, double* out) {
+  publish_values_kernel<<<1, 1024, 0, st>>>(part, nb, pstride, count, slots, rank,
+                                            X.active() ? X.ds->sig_all : Signal{},
+                                            X.active() ? X.ds->d_peer_slots : nullptr);
+  X.wait_all(st);
+  sum_slots_kernel<<<1, 32, 0, st>>>(slots, world, count, out);
+  X.nl += 2;
+  TECCL_CHECK_LAUNCH();
+  return TECCL_OK;
+}
 
 template <bool UNIT, bool DICT>
 int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x_dev,
@@ -659,6 +915,14 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
   cudaStream_t st = ctx->stream;
   const int32_t m = lp->m, n = lp->n;
   const int nb_row = (int)((m + kTile - 1) / kTile), nb_col = (int)((n + kTile - 1) / kTile);
+  DistState* ds = (DistState*)lp->dist;
+  if (lp->part_world > 1 && (!ds || !ds->connected)) {
+    set_error("partitioned LP: call teccl_dist_export/teccl_dist_connect before solving");
+    return TECCL_EINVAL;
+  }
+  const int world = ds ? ds->world : 1, rank = ds ? ds->rank : 0;
+  const int64_t ncw = gather_cols(lp), nrw = gather_rows(lp);
+  const int64_t oc = own_col_off(lp), orr = own_row_off(lp);
   Workspace* ws = (Workspace*)lp->pdlp_ws;
   if (!ws) {
     ws = new Workspace();
@@ -666,17 +930,26 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
     ws->st = st;
     Workspace& W = *ws;
     W.pstride = std::max<int64_t>(std::max(nb_row, nb_col), kGrid);
-    W.R = W.alloc<double>(m + 1); W.C = W.alloc<double>(n + 1);
     W.rstat = W.alloc<double>(m); W.cstat = W.alloc<double>(n);
     W.D = W.alloc<float>(n); W.E = W.alloc<float>(m);
     W.x0 = W.alloc<float>(n); W.y0 = W.alloc<float>(m);
-    W.x = W.alloc<double>(n); W.xt = W.alloc<double>(n + 1); W.xbar = W.alloc<double>(n + 1);
-    W.y = W.alloc<double>(m + 1); W.yt = W.alloc<double>(m + 1);
+    W.x = W.alloc<double>(n);
+    if (!ds) {  // single device: the gather windows are the owned vectors
+      W.R = W.alloc<double>(m + 1); W.C = W.alloc<double>(n + 1);
+      W.xt = W.alloc<double>(n + 1); W.xbar = W.alloc<double>(n + 1);
+      W.y = W.alloc<double>(m + 1); W.yt = W.alloc<double>(m + 1);
+      W.slots = W.alloc<double>(kSlots);
+    } else {
+      W.R = ds->arr(A_RW); W.C = ds->arr(A_CW);
+      W.xt = ds->arr(A_XT); W.xbar = ds->arr(A_XBAR);
+      W.y = ds->arr(A_Y); W.yt = ds->arr(A_YT);
+      W.slots = ds->slots();
+    }
     W.part = W.alloc<double>((int64_t)kNQ * W.pstride);
     W.part2 = W.alloc<double>(kGrid);
     W.dst = W.alloc<PdlpState>(1);
     const bool ok = W.R && W.C && W.rstat && W.cstat && W.D && W.E && W.x0 && W.y0 && W.x &&
-                    W.xt && W.xbar && W.y && W.yt && W.part && W.part2 && W.dst;
+                    W.xt && W.xbar && W.y && W.yt && W.part && W.part2 && W.dst && W.slots;
     if (!ok || cudaEventCreate(&W.ev0) != cudaSuccess || cudaEventCreate(&W.ev1) != cudaSuccess) {
       delete ws;
       set_error("device allocation failed for PDLP workspace");
@@ -693,45 +966,59 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
   auto mark = [&](const char* what) {
     if (trace) {
       cudaStreamSynchronize(st);
-      fprintf(stderr, "[teccl trace] %-14s %8.3f ms\n", what,
+      fprintf(stderr, "[teccl trace r%d] %-14s %8.3f ms\n", rank, what,
               std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count());
     }
   };
   const int64_t pstride = W.pstride;
-  double *R = W.R, *C = W.C, *rstat = W.rstat, *cstat = W.cstat;
+  // window (gathered) arrays and their owned parts
+  double *R_w = W.R, *C_w = W.C, *xt_w = W.xt, *xbar_w = W.xbar, *y_w = W.y, *yt_w = W.yt;
+  double *R = R_w + orr, *C = C_w + oc;
+  double *xt = xt_w + oc, *xbar = xbar_w + oc, *y = y_w + orr, *yt = yt_w + orr;
+  double *rstat = W.rstat, *cstat = W.cstat;
   float *D = W.D, *E = W.E, *x0 = W.x0, *y0 = W.y0;
-  double *x = W.x, *xt = W.xt, *xbar = W.xbar, *y = W.y, *yt = W.yt;
-  double *part = W.part, *part2 = W.part2;
+  double* x = W.x;
+  double *part = W.part, *part2 = W.part2, *slots = W.slots;
   PdlpState* dst = W.dst;
+  Exchange X;
+  X.ds = ds;
+  X.st = dst;
+  TECCL_CUDA(cudaMemsetAsync(dst, 0, sizeof(PdlpState), st));
   TECCL_CUDA(cudaMemsetAsync(part, 0, sizeof(double) * kNQ * pstride, st));
-  // always-zero slots the SELL padding gathers from
-  TECCL_CUDA(cudaMemsetAsync(xt, 0, sizeof(double) * (n + 1), st));
-  TECCL_CUDA(cudaMemsetAsync(xbar, 0, sizeof(double) * (n + 1), st));
-  TECCL_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * (m + 1), st));
-  TECCL_CUDA(cudaMemsetAsync(yt, 0, sizeof(double) * (m + 1), st));
+  // always-zero slots the SELL padding gathers from (index = window length)
+  TECCL_CUDA(cudaMemsetAsync(xt_w, 0, sizeof(double) * (ncw + 1), st));
+  TECCL_CUDA(cudaMemsetAsync(xbar_w, 0, sizeof(double) * (ncw + 1), st));
+  TECCL_CUDA(cudaMemsetAsync(y_w, 0, sizeof(double) * (nrw + 1), st));
+  TECCL_CUDA(cudaMemsetAsync(yt_w, 0, sizeof(double) * (nrw + 1), st));
   {
     int rc = teccl_build_sell(lp, st);
     if (rc) return rc;
   }
-  const int gr = grid_for(m > n ? m : n);
+  if (X.active()) {  // every rank has finished resetting before anyone writes peer memory
+    publish_values_kernel<<<1, 1024, 0, st>>>(part, 1, pstride, 0, slots, rank, ds->sig_all,
+                                              ds->d_peer_slots);
+    X.wait_all(st);
+  }
+  const int gr = grid_for(std::max<int64_t>(std::max<int64_t>(m, n), std::max(ncw, nrw)));
   int64_t nl = 0;  // kernel launches issued by this solve
   mark("setup+sell");
 
   // --- Ruiz equilibration + Pock-Chambolle (alpha = 1), simultaneous updates
-  fill_kernel<<<gr, kThreads, 0, st>>>(m, R, 1.0);
-  fill_kernel<<<gr, kThreads, 0, st>>>(n, C, 1.0);
+  fill_kernel<<<gr, kThreads, 0, st>>>(nrw, R_w, 1.0);
+  fill_kernel<<<gr, kThreads, 0, st>>>(ncw, C_w, 1.0);
   nl += 2;
   for (int it = 0; it <= o->ruiz_iters; ++it) {
     if (it < o->ruiz_iters) {
-      abs_stat_kernel<UNIT, true><<<gr, kThreads, 0, st>>>(m, lp->row_ptr, lp->col, lp->val, C, R, rstat);
-      abs_stat_kernel<UNIT, true><<<gr, kThreads, 0, st>>>(n, lp->col_ptr, lp->row, lp->cval, R, C, cstat);
+      abs_stat_kernel<UNIT, true><<<gr, kThreads, 0, st>>>(m, lp->row_ptr, lp->col, lp->val, C_w, R, rstat);
+      abs_stat_kernel<UNIT, true><<<gr, kThreads, 0, st>>>(n, lp->col_ptr, lp->row, lp->cval, R_w, C, cstat);
     } else {
-      abs_stat_kernel<UNIT, false><<<gr, kThreads, 0, st>>>(m, lp->row_ptr, lp->col, lp->val, C, R, rstat);
-      abs_stat_kernel<UNIT, false><<<gr, kThreads, 0, st>>>(n, lp->col_ptr, lp->row, lp->cval, R, C, cstat);
+      abs_stat_kernel<UNIT, false><<<gr, kThreads, 0, st>>>(m, lp->row_ptr, lp->col, lp->val, C_w, R, rstat);
+      abs_stat_kernel<UNIT, false><<<gr, kThreads, 0, st>>>(n, lp->col_ptr, lp->row, lp->cval, R_w, C, cstat);
     }
     apply_scale_kernel<<<gr, kThreads, 0, st>>>(m, R, rstat);
     apply_scale_kernel<<<gr, kThreads, 0, st>>>(n, C, cstat);
     nl += 4;
+    X.halo(st, {A_CW, A_RW});
   }
   TECCL_CHECK_LAUNCH();
 
@@ -745,39 +1032,43 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
 
   // --- norms: scaled ||C c||, ||R b|| set the initial primal weight (the
   // bound/objective rescaling of PDLP); unscaled ||c||, ||b|| enter the
-  // relative termination criteria
-  double csq_s = 0.0, csq_u = 0.0, bsq_s = 0.0, bsq_u = 0.0;
-  norms_kernel<<<kGrid, kThreads, 0, st>>>(n, C, lp->obj, nullptr, 0, part, part2);
-  if (read_partials(part, kGrid, st, &csq_s) || read_partials(part2, kGrid, st, &csq_u)) return TECCL_ECUDA;
-  norms_kernel<<<kGrid, kThreads, 0, st>>>(m, R, lp->row_lo, lp->row_hi, 1, part, part2);
-  if (read_partials(part, kGrid, st, &bsq_s) || read_partials(part2, kGrid, st, &bsq_u)) return TECCL_ECUDA;
+  // relative termination criteria. Global sums over ranks.
+  double nrm[8] = {0};
+  norms_kernel<<<kGrid, kThreads, 0, st>>>(n, C, lp->obj, nullptr, 0, part, part + pstride);
+  norms_kernel<<<kGrid, kThreads, 0, st>>>(m, R, lp->row_lo, lp->row_hi, 1, part + 2 * pstride,
+                                           part + 3 * pstride);
   nl += 2;
+  if (all_reduce(st, X, part, kGrid, pstride, 4, slots, world, rank, part2)) return TECCL_ECUDA;
+  TECCL_CUDA(cudaMemcpyAsync(nrm, part2, sizeof(double) * 8, cudaMemcpyDeviceToHost, st));
+  TECCL_CUDA(cudaStreamSynchronize(st));
+  const double csq_s = nrm[0], csq_u = nrm[1], bsq_s = nrm[2], bsq_u = nrm[3];
   const double beta = sqrt(bsq_s) + 1.0, gamma = sqrt(csq_s) + 1.0;
   const double cn_s = sqrt(csq_s) / gamma, bn_s = sqrt(bsq_s) / beta;
   const double omega_s = (cn_s > 1e-10 && bn_s > 1e-10) ? cn_s / bn_s : 1.0;
 
   // --- power iteration for ||E^1/2 A D^1/2||_2 (v in xt, D^1/2 v in xbar,
-  // A D^1/2 v in yt, E A D^1/2 v in y)
+  // A D^1/2 v in yt, E A D^1/2 v in y); norms reduced on the device
   double sigma_max = 1.0;
-  if (m > 0 && n > 0 && lp->nnz > 0) {
-    // 40 rounds fully on the device (norms reduced and applied by kernels);
-    // one host read at the end
-    double* scal = part2;  // part2[0..1]: squared norm, inverse norm
+  {
+    double* scal = part2;  // [0] squared norm, [1] inverse norm
     hash_fill_kernel<<<gr, kThreads, 0, st>>>(n, xt);
     sumsq_kernel<<<kGrid, kThreads, 0, st>>>(n, xt, part);
-    finalize_norm_kernel<<<1, 1024, 0, st>>>(part, kGrid, scal);
+    nl += 2;
+    if (all_reduce(st, X, part, kGrid, pstride, 1, slots, world, rank, scal)) return TECCL_ECUDA;
     scale_by_kernel<<<gr, kThreads, 0, st>>>(n, xt, scal);
-    nl += 4;
+    nl += 1;
     const int rounds = 40;
     for (int it = 0; it < rounds; ++it) {
       mul_kernel<<<gr, kThreads, 0, st>>>(n, xbar, xt, rootD);
-      spmv_scaled_kernel<UNIT><<<gr, kThreads, 0, st>>>(m, lp->row_ptr, lp->col, lp->val, xbar, nullptr, yt);
+      X.halo(st, {A_XBAR});
+      spmv_scaled_kernel<UNIT><<<gr, kThreads, 0, st>>>(m, lp->row_ptr, lp->col, lp->val, xbar_w, nullptr, yt);
       mul_kernel<<<gr, kThreads, 0, st>>>(m, y, yt, rootE);
       mul_kernel<<<gr, kThreads, 0, st>>>(m, y, y, rootE);
-      spmv_scaled_kernel<UNIT><<<gr, kThreads, 0, st>>>(n, lp->col_ptr, lp->row, lp->cval, y, rootD, xt);
+      X.halo(st, {A_Y});
+      spmv_scaled_kernel<UNIT><<<gr, kThreads, 0, st>>>(n, lp->col_ptr, lp->row, lp->cval, y_w, rootD, xt);
       sumsq_kernel<<<kGrid, kThreads, 0, st>>>(n, xt, part);
-      finalize_norm_kernel<<<1, 1024, 0, st>>>(part, kGrid, scal);
-      nl += 7;
+      nl += 6;
+      if (all_reduce(st, X, part, kGrid, pstride, 1, slots, world, rank, scal)) return TECCL_ECUDA;
       if (it + 1 < rounds) {
         scale_by_kernel<<<gr, kThreads, 0, st>>>(n, xt, scal);
         nl += 1;
@@ -787,10 +1078,10 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
     TECCL_CUDA(cudaMemcpyAsync(&nv, scal, sizeof(double), cudaMemcpyDeviceToHost, st));
     TECCL_CUDA(cudaStreamSynchronize(st));
     if (nv > 0.0 && std::isfinite(nv)) sigma_max = sqrt(sqrt(nv));
-    TECCL_CUDA(cudaMemsetAsync(xbar, 0, sizeof(double) * (n + 1), st));
-    TECCL_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * (m + 1), st));
-    TECCL_CUDA(cudaMemsetAsync(xt, 0, sizeof(double) * (n + 1), st));
-    TECCL_CUDA(cudaMemsetAsync(yt, 0, sizeof(double) * (m + 1), st));
+    TECCL_CUDA(cudaMemsetAsync(xbar_w, 0, sizeof(double) * (ncw + 1), st));
+    TECCL_CUDA(cudaMemsetAsync(y_w, 0, sizeof(double) * (nrw + 1), st));
+    TECCL_CUDA(cudaMemsetAsync(xt_w, 0, sizeof(double) * (ncw + 1), st));
+    TECCL_CUDA(cudaMemsetAsync(yt_w, 0, sizeof(double) * (nrw + 1), st));
   }
   TECCL_CHECK_LAUNCH();
 
@@ -817,16 +1108,25 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
   V.D = D; V.E = E;
   V.col = Bounds{lp->col_code, lp->col_dict, lp->var_lb, lp->var_ub, lp->obj};
   V.row = Bounds{lp->row_code, lp->row_dict, lp->row_lo, lp->row_hi, nullptr};
-  V.x = x; V.xt = xt; V.xbar = xbar; V.x0 = x0;
-  V.y = y; V.yt = yt; V.y0 = y0;
+  V.x = x; V.x0 = x0; V.y0 = y0;
   V.c_u = lp->obj; V.lb_u = lp->var_lb; V.ub_u = lp->var_ub; V.lo_u = lp->row_lo; V.hi_u = lp->row_hi;
   V.part = part;
   V.pstride = pstride;
   V.nb_row = nb_row;
   V.nb_col = nb_col;
   V.st = dst;
-  init_iterates_kernel<<<gr, kThreads, 0, st>>>(n, m, V, o->warm_start, x_dev, y_dev);
+  V.slots = slots;
+  V.world = world;
+  V.rank = rank;
+  // Vc: column kernels (own x side, gather y windows); Vr: row kernels
+  // (own y side, gather x windows); Vi: owned parts only
+  Vecs Vc = V, Vr = V, Vi = V;
+  Vc.xt = xt; Vc.xbar = xbar; Vc.y = y_w; Vc.yt = yt_w;
+  Vr.y = y; Vr.yt = yt; Vr.xbar = xbar_w; Vr.xt = xt_w;
+  Vi.xt = xt; Vi.xbar = xbar; Vi.y = y; Vi.yt = yt;
+  init_iterates_kernel<<<gr, kThreads, 0, st>>>(n, m, Vi, o->warm_start, x_dev, y_dev);
   nl += 1;
+  if (o->warm_start) X.halo(st, {A_Y, A_YT});
   TECCL_CHECK_LAUNCH();
 
   if (sb) {  // time the fused iteration kernels alone, CUDA events on this stream
@@ -835,13 +1135,13 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
     TECCL_CUDA(cudaEventCreate(&b));
     TECCL_CUDA(cudaEventCreate(&c2));
     for (int w = 0; w < 3; ++w) {
-      launch_col<UNIT, DICT, false>(st, lp, V, 0);
-      launch_row<UNIT, DICT, false>(st, lp, V, 0);
+      launch_col<UNIT, DICT, false>(st, lp, Vc, 0);
+      launch_row<UNIT, DICT, false>(st, lp, Vr, 0);
     }
     TECCL_CUDA(cudaEventRecord(a, st));
-    for (int r = 0; r < sb->reps; ++r) launch_col<UNIT, DICT, false>(st, lp, V, 0);
+    for (int r = 0; r < sb->reps; ++r) launch_col<UNIT, DICT, false>(st, lp, Vc, 0);
     TECCL_CUDA(cudaEventRecord(b, st));
-    for (int r = 0; r < sb->reps; ++r) launch_row<UNIT, DICT, false>(st, lp, V, 0);
+    for (int r = 0; r < sb->reps; ++r) launch_row<UNIT, DICT, false>(st, lp, Vr, 0);
     TECCL_CUDA(cudaEventRecord(c2, st));
     TECCL_CHECK_LAUNCH();
     TECCL_CUDA(cudaEventSynchronize(c2));
@@ -856,9 +1156,9 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
     const double ns_c = (double)((n + 31) / 32), ns_r = (double)((m + 31) / 32);
     const double cb = DICT ? 2.0 : 24.0, rbd = DICT ? 2.0 : 16.0;
     // column: x(8) x0(4) D(4) bounds(cb) read; x(8) xbar(8) written
-    sb->bytes_col = 12.0 * ns_c + ib * lp->scol_entries + 8.0 * m + (32.0 + cb) * n;
+    sb->bytes_col = 12.0 * ns_c + ib * lp->scol_entries + 8.0 * nrw + (32.0 + cb) * n;
     // row: y(8) y0(4) E(4) bounds(rbd) read; y(8) written
-    sb->bytes_row = 12.0 * ns_r + ib * lp->srow_entries + 8.0 * n + (24.0 + rbd) * m;
+    sb->bytes_row = 12.0 * ns_r + ib * lp->srow_entries + 8.0 * ncw + (24.0 + rbd) * m;
     cudaEventDestroy(a); cudaEventDestroy(b); cudaEventDestroy(c2);
     return TECCL_OK;
   }
@@ -868,12 +1168,15 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
     cudaGraphExecDestroy(W.gexec);
     W.gexec = nullptr;
   }
+  const int64_t nl_setup = nl + X.nl;
+  X.nl = 0;
+  int64_t per_chunk = 0;
   if (o->use_graphs && !W.gexec) {
     cudaGraph_t g;
     cudaStream_t cap;
     TECCL_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
     TECCL_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
-    enqueue_chunk<UNIT, DICT>(chunk, cap, lp, V);
+    enqueue_chunk<UNIT, DICT>(chunk, cap, lp, Vc, Vr, X, y_w, yt_w);
     TECCL_CUDA(cudaStreamEndCapture(cap, &g));
     TECCL_CUDA(cudaGraphInstantiate(&W.gexec, g, 0));
     TECCL_CUDA(cudaGraphDestroy(g));
@@ -881,8 +1184,9 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
     W.graph_chunk = chunk;
   }
   cudaGraphExec_t gexec = o->use_graphs ? W.gexec : nullptr;
-
+  per_chunk = 2LL * chunk + 6 + (X.active() ? 4LL * chunk + 1 : 0);
   mark("graph");
+
   // --- iterate: chunks queued `lookahead` deep; the device stops itself
   const int look = o->lookahead > 0 ? o->lookahead : 1;
   if (W.ring_len < look) {
@@ -908,7 +1212,7 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
       if (gexec) {
         TECCL_CUDA(cudaGraphLaunch(gexec, st));
       } else {
-        enqueue_chunk<UNIT, DICT>(chunk, st, lp, V);
+        enqueue_chunk<UNIT, DICT>(chunk, st, lp, Vc, Vr, X, y_w, yt_w);
       }
       TECCL_CHECK_LAUNCH();
       const int slot = (int)(launched % look);
@@ -922,18 +1226,19 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
     last = ring[slot];
     ++polled;
     if (o->verbose > 0 && (polled % o->verbose == 0 || last.done))
-      fprintf(stderr, "[teccl pdlp] it=%lld rp=%.2e rd=%.2e gap=%.2e pobj=%.9g w=%.3e r=%.2e restarts=%d\n",
-              last.total, last.rel_p, last.rel_d, last.gap, last.pobj, last.omega, last.last_r,
+      fprintf(stderr, "[teccl pdlp r%d] it=%lld rp=%.2e rd=%.2e gap=%.2e pobj=%.9g w=%.3e r=%.2e restarts=%d\n",
+              rank, last.total, last.rel_p, last.rel_d, last.gap, last.pobj, last.omega, last.last_r,
               last.restarts);
     if (last.done == 1) { status = TECCL_OPTIMAL; stop = true; }
     else if (last.done == 2) { status = TECCL_NUMERICAL; stop = true; }
+    else if (last.done == 4) { status = TECCL_PEER_TIMEOUT; stop = true; }
     else if (polled >= max_chunks) { status = TECCL_ITER_LIMIT; stop = true; }
-    else {
+    else if (!X.active()) {  // ranks must stop together: only iteration caps in multi-GPU
       const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
       if (el > o->time_limit) { status = TECCL_TIME_LIMIT; stop = true; }
     }
   }
-  if (status != TECCL_OPTIMAL && status != TECCL_NUMERICAL) {
+  if (status == TECCL_ITER_LIMIT || status == TECCL_TIME_LIMIT) {
     // stop anything still queued from touching the iterates
     static const int kStopped = 3;
     TECCL_CUDA(cudaMemcpyAsync(&dst->done, &kStopped, sizeof(int), cudaMemcpyHostToDevice, st));
@@ -944,8 +1249,7 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
   if (last.done == 3) last.done = 0;
 
   mark("iterate");
-  output_kernel<<<gr, kThreads, 0, st>>>(n, m, V, x_dev, y_dev);
-  nl += 1;
+  output_kernel<<<gr, kThreads, 0, st>>>(n, m, Vi, x_dev, y_dev);
   TECCL_CHECK_LAUNCH();
   TECCL_CUDA(cudaEventRecord(ev1, st));
   TECCL_CUDA(cudaEventSynchronize(ev1));
@@ -964,7 +1268,7 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
   res->solve_seconds = ms * 1e-3;
   res->omega = last.omega;
   res->step = hs.eta;
-  res->spmv_launches = nl + launched * (2LL * chunk + 5);
+  res->spmv_launches = nl_setup + 1 + launched * per_chunk;
   return TECCL_OK;
 }
 
@@ -1092,5 +1396,109 @@ extern "C" int teccl_spmv_bench(teccl_ctx* ctx, teccl_lp* lp, int32_t reps, doub
   cudaFreeAsync(vx, st);
   cudaFreeAsync(vy, st);
   TECCL_CUDA(cudaStreamSynchronize(st));
+  return TECCL_OK;
+}
+
+extern "C" int teccl_dist_export(teccl_ctx* ctx, teccl_lp* lp, uint8_t* blob, int64_t* blob_len) {
+  if (!ctx || !lp || !blob || !blob_len) { set_error("null argument"); return TECCL_EINVAL; }
+  if (lp->part_world < 2) { set_error("LP is not row-partitioned"); return TECCL_EINVAL; }
+  TECCL_CUDA(cudaSetDevice(ctx->device));
+  DistState* ds = (DistState*)lp->dist;
+  if (!ds) {
+    ds = new DistState();
+    ds->world = lp->part_world;
+    ds->rank = lp->part_rank;
+    ds->device = ctx->device;
+    const int64_t ncw = gather_cols(lp), nrw = gather_rows(lp);
+    auto al = [](int64_t b) { return (b + 255) / 256 * 256; };
+    int64_t off = 0;
+    ds->meta[M_NCW] = ncw;
+    ds->meta[M_NRW] = nrw;
+    for (int id = 0; id < A_NARR; ++id) {
+      ds->meta[M_OFF0 + id] = off;
+      off += al(8 * ((ds->is_col(id) ? ncw : nrw) + 1));
+    }
+    ds->meta[M_FLAGS] = off; off += al(8 * ds->world);
+    ds->meta[M_SLOTS] = off; off += al(8 * kSlots * ds->world);
+    ds->meta[M_SEQ] = off; off += 256;
+    ds->meta[M_ARRIVE] = off; off += 256;
+    ds->meta[M_OC0] = lp->own_c0; ds->meta[M_OC1] = lp->own_c1;
+    ds->meta[M_OR0] = lp->own_r0; ds->meta[M_OR1] = lp->own_r1;
+    ds->meta[M_WC0] = lp->win_c0; ds->meta[M_WC1] = lp->win_c1;
+    ds->meta[M_WR0] = lp->win_r0; ds->meta[M_WR1] = lp->win_r1;
+    ds->meta[M_RANK] = ds->rank;
+    ds->meta[M_WORLD] = ds->world;
+    if (cudaMalloc((void**)&ds->arena, off) != cudaSuccess) {
+      delete ds;
+      set_error("cannot allocate the peer-exchange arena");
+      return TECCL_ENOMEM;
+    }
+    TECCL_CUDA(cudaMemset(ds->arena, 0, off));
+    lp->dist = ds;
+    lp->dist_free = free_dist;
+  }
+  cudaIpcMemHandle_t h;
+  TECCL_CUDA(cudaIpcGetMemHandle(&h, ds->arena));
+  memcpy(blob, &h, sizeof(h));
+  memcpy(blob + sizeof(h), ds->meta, kMetaLen * 8);
+  *blob_len = kBlobLen;
+  return TECCL_OK;
+}
+
+extern "C" int teccl_dist_connect(teccl_ctx* ctx, teccl_lp* lp, const uint8_t* blobs,
+                                  int64_t blob_len) {
+  if (!ctx || !lp || !blobs || blob_len != kBlobLen) { set_error("bad argument"); return TECCL_EINVAL; }
+  DistState* ds = (DistState*)lp->dist;
+  if (!ds) { set_error("call teccl_dist_export first"); return TECCL_EINVAL; }
+  TECCL_CUDA(cudaSetDevice(ctx->device));
+  const int W = ds->world, me = ds->rank;
+  ds->peer_meta.assign(W, {});
+  ds->peer_base.assign(W, nullptr);
+  for (int q = 0; q < W; ++q) {
+    const uint8_t* b = blobs + (int64_t)q * kBlobLen;
+    memcpy(ds->peer_meta[q].data(), b + sizeof(cudaIpcMemHandle_t), kMetaLen * 8);
+    if (ds->peer_meta[q][M_RANK] != q || ds->peer_meta[q][M_WORLD] != W) {
+      set_error("peer blobs out of rank order or from another world");
+      return TECCL_EINVAL;
+    }
+    if (q == me) continue;
+    cudaIpcMemHandle_t h;
+    memcpy(&h, b, sizeof(h));
+    void* ptr = nullptr;
+    TECCL_CUDA(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    ds->peer_base[q] = (char*)ptr;
+  }
+  std::vector<double*> ps;
+  int na = 0;
+  for (int q = 0; q < W; ++q) {
+    if (q == me) continue;
+    char* base = ds->peer_base[q];
+    unsigned long long* their_flag = (unsigned long long*)(base + ds->peer_meta[q][M_FLAGS]) + me;
+    ps.push_back((double*)(base + ds->peer_meta[q][M_SLOTS]));
+    if (na < kMaxPeers) {
+      ds->sig_all.peer_flag[na] = their_flag;
+      ds->wait_all.peer[na] = q;
+      ++na;
+    }
+    if (q == me - 1 || q == me + 1) {
+      ds->sig_nbr.peer_flag[ds->sig_nbr.npeer++] = their_flag;
+      ds->wait_nbr.peer[ds->wait_nbr.npeer++] = q;
+    }
+  }
+  if (W - 1 > kMaxPeers) { set_error("more than 9 ranks are not supported"); return TECCL_EINVAL; }
+  ds->sig_all.npeer = na;
+  ds->wait_all.npeer = na;
+  unsigned long long* seq = (unsigned long long*)(ds->arena + ds->meta[M_SEQ]);
+  unsigned int* arrive = (unsigned int*)(ds->arena + ds->meta[M_ARRIVE]);
+  const unsigned long long* flags = (const unsigned long long*)(ds->arena + ds->meta[M_FLAGS]);
+  ds->sig_nbr.seq = ds->sig_all.seq = seq;
+  ds->sig_nbr.arrive = ds->sig_all.arrive = arrive;
+  ds->wait_nbr.flags = ds->wait_all.flags = flags;
+  ds->wait_nbr.seq = ds->wait_all.seq = seq;
+  if (ds->d_peer_slots) cudaFree(ds->d_peer_slots);
+  TECCL_CUDA(cudaMalloc((void**)&ds->d_peer_slots, sizeof(double*) * std::max<size_t>(1, ps.size())));
+  if (!ps.empty())
+    TECCL_CUDA(cudaMemcpy(ds->d_peer_slots, ps.data(), sizeof(double*) * ps.size(), cudaMemcpyHostToDevice));
+  ds->connected = true;
   return TECCL_OK;
 }

@@ -91,10 +91,10 @@ static int build_one(int64_t count, const int64_t* ptr, const uint32_t* idx, con
 int teccl_build_sell(teccl_lp* lp, cudaStream_t st) {
   using namespace teccl;
   if (lp->sell_ready) return TECCL_OK;
-  int rc = build_one(lp->m, lp->row_ptr, lp->col, lp->unit ? nullptr : lp->val, (uint32_t)lp->n,
+  int rc = build_one(lp->m, lp->row_ptr, lp->col, lp->unit ? nullptr : lp->val, (uint32_t)gather_cols(lp),
                      st, &lp->srow_off, &lp->srow_w, &lp->srow_idx, &lp->srow_val, &lp->srow_entries);
   if (rc) return rc;
-  rc = build_one(lp->n, lp->col_ptr, lp->row, lp->unit ? nullptr : lp->cval, (uint32_t)lp->m, st,
+  rc = build_one(lp->n, lp->col_ptr, lp->row, lp->unit ? nullptr : lp->cval, (uint32_t)gather_rows(lp), st,
                  &lp->scol_off, &lp->scol_w, &lp->scol_idx, &lp->scol_val, &lp->scol_entries);
   if (rc) return rc;
   TECCL_CUDA(cudaStreamSynchronize(st));

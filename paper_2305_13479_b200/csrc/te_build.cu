@@ -81,88 +81,99 @@ struct Emitter {
 };
 
 // ---------------------------------------------------------------------------
-// Row generator: one thread per row; counts (FILL=false) or writes the row.
+// Row generator. gen_row emits reference row r's entries (reference column
+// ids, ascending) into `em` and returns its bounds and bound class; the
+// kernels below run it one thread per row, twice (count, then fill).
+template <class Em>
+__device__ __forceinline__ void gen_row(const TeDev& d, int64_t r, Em& em, double& rlo, double& rhi,
+                                        int& rc) {
+  const int K = d.K;
+  rlo = 0.0;
+  rhi = 0.0;
+  rc = 0;                                          // bound class: 0 = (0,0)
+  if (r < d.S) {                                   // init(s), lp.py:69-72
+    int s = (int)r, n = d.snode[s];
+    for (int j = d.out_ptr[n]; j < d.out_ptr[n + 1]; ++j) em.put(varF(d, s, d.out_e[j], 0), false);
+    em.put(varB(d, s, d.gpu_of[n], 0), false);
+    rlo = rhi = d.out_units[s];
+    if (d.dict_row) rc = 1 + d.src_ouidx[s];
+  } else if (r < d.R_cons) {                       // cap(e,k), lp.py:74-77
+    int64_t q = r - d.S;
+    int e = (int)(q / K), k = (int)(q % K);
+    for (int s = 0; s < d.S; ++s) em.put(varF(d, s, e, k), false);
+    rlo = -INFINITY;
+    rhi = d.ecap[(int64_t)e * K + k];
+    if (d.dict_row) rc = 1 + d.nOU + d.cap_idx[q];
+  } else if (r < d.R_cum) {                        // cons / last, lp.py:81-116
+    int64_t q = r - d.R_cons;
+    int s = (int)(q / d.CB);
+    int64_t off = q % d.CB;
+    // node n: last node with cons_off(s,n) <= off (offsets ascend with n)
+    int lo_n = 0, hi_n = d.Nn - 1;
+    while (lo_n < hi_n) {
+      int mid = (lo_n + hi_n + 1) >> 1;
+      if (cons_off(d, s, mid) <= off) lo_n = mid; else hi_n = mid - 1;
+    }
+    int n = lo_n;
+    int k = (int)(off - cons_off(d, s, n));      // k == K marks the last row
+    int g = d.gpu_of[n];
+    int pair = (g >= 0) ? d.pair_of[s * d.Nn + n] : -1;
+    if (k < K) {
+      for (int j = d.inc_ptr[n]; j < d.inc_ptr[n + 1]; ++j) {
+        uint32_t t = d.inc[j];
+        int e = (int)(t & kIdxMask);
+        if (t & kSignBit) {                        // leaves n: send next epoch
+          if (k + 1 <= K - 1) em.put(varF(d, s, e, k + 1), true);
+        } else {                                   // arrives at n
+          int kin = k - d.edelta[e];
+          if (kin >= 0) em.put(varF(d, s, e, kin), false);
+        }
+      }
+      if (g >= 0) {
+        em.put(varB(d, s, g, k), false);
+        em.put(varB(d, s, g, k + 1), true);
+        if (pair >= 0) em.put(varRd(d, pair, k), true);
+      }
+    } else {                                       // last(s,n), lp.py:107-116
+      for (int j = d.inc_ptr[n]; j < d.inc_ptr[n + 1]; ++j) {
+        uint32_t t = d.inc[j];
+        if (t & kSignBit) continue;
+        int e = (int)(t & kIdxMask);
+        int kin = K - 1 - d.edelta[e];
+        if (kin >= 0) em.put(varF(d, s, e, kin), false);
+      }
+      if (pair >= 0) em.put(varRd(d, pair, K - 1), true);
+    }
+    rlo = rhi = 0.0;
+  } else if (r < d.R_bcap) {                       // cum(p,k), lp.py:118-123
+    int64_t q = r - d.R_cum;
+    int p = (int)(q / K), k = (int)(q % K);
+    int64_t rd = varRd(d, p, k);
+    if (k >= 1) em.put(rd - 1, true);              // Rc(p,k-1)
+    em.put(rd, true);                              // Rd(p,k)
+    em.put(rd + 1, false);                         // Rc(p,k)
+    rlo = rhi = 0.0;
+  } else {                                         // bcap(g,k), lp.py:125-131
+    int64_t q = r - d.R_bcap;
+    int g = (int)(q / (K + 1)), k = (int)(q % (K + 1));
+    for (int s = 0; s < d.S; ++s) em.put(varB(d, s, g, k), false);
+    rlo = -INFINITY;
+    rhi = d.blimit;
+    rc = 1 + d.nOU + d.nCap;
+  }
+}
+
 template <bool FILL>
 __global__ void te_rows_kernel(TeDev d, const int64_t* __restrict__ row_ptr,
                                uint32_t* __restrict__ col, int64_t* __restrict__ row_len,
                                double* __restrict__ lo, double* __restrict__ hi,
                                uint16_t* __restrict__ code) {
-  const int K = d.K;
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < d.n_rows;
        r += (int64_t)gridDim.x * blockDim.x) {
     Emitter<FILL> em{FILL ? col + row_ptr[r] : nullptr, 0};
-    double rlo = 0.0, rhi = 0.0;
-    int rc = 0;                                      // bound class: 0 = (0,0)
-    if (r < d.S) {                                   // init(s), lp.py:69-72
-      int s = (int)r, n = d.snode[s];
-      for (int j = d.out_ptr[n]; j < d.out_ptr[n + 1]; ++j) em.put(varF(d, s, d.out_e[j], 0), false);
-      em.put(varB(d, s, d.gpu_of[n], 0), false);
-      rlo = rhi = d.out_units[s];
-      if (d.dict_row) rc = 1 + d.src_ouidx[s];
-    } else if (r < d.R_cons) {                       // cap(e,k), lp.py:74-77
-      int64_t q = r - d.S;
-      int e = (int)(q / K), k = (int)(q % K);
-      for (int s = 0; s < d.S; ++s) em.put(varF(d, s, e, k), false);
-      rlo = -INFINITY;
-      rhi = d.ecap[(int64_t)e * K + k];
-      if (d.dict_row) rc = 1 + d.nOU + d.cap_idx[q];
-    } else if (r < d.R_cum) {                        // cons / last, lp.py:81-116
-      int64_t q = r - d.R_cons;
-      int s = (int)(q / d.CB);
-      int64_t off = q % d.CB;
-      // node n: last node with cons_off(s,n) <= off (offsets ascend with n)
-      int lo_n = 0, hi_n = d.Nn - 1;
-      while (lo_n < hi_n) {
-        int mid = (lo_n + hi_n + 1) >> 1;
-        if (cons_off(d, s, mid) <= off) lo_n = mid; else hi_n = mid - 1;
-      }
-      int n = lo_n;
-      int k = (int)(off - cons_off(d, s, n));      // k == K marks the last row
-      int g = d.gpu_of[n];
-      int pair = (g >= 0) ? d.pair_of[s * d.Nn + n] : -1;
-      if (k < K) {
-        for (int j = d.inc_ptr[n]; j < d.inc_ptr[n + 1]; ++j) {
-          uint32_t t = d.inc[j];
-          int e = (int)(t & kIdxMask);
-          if (t & kSignBit) {                        // leaves n: send next epoch
-            if (k + 1 <= K - 1) em.put(varF(d, s, e, k + 1), true);
-          } else {                                   // arrives at n
-            int kin = k - d.edelta[e];
-            if (kin >= 0) em.put(varF(d, s, e, kin), false);
-          }
-        }
-        if (g >= 0) {
-          em.put(varB(d, s, g, k), false);
-          em.put(varB(d, s, g, k + 1), true);
-          if (pair >= 0) em.put(varRd(d, pair, k), true);
-        }
-      } else {                                       // last(s,n), lp.py:107-116
-        for (int j = d.inc_ptr[n]; j < d.inc_ptr[n + 1]; ++j) {
-          uint32_t t = d.inc[j];
-          if (t & kSignBit) continue;
-          int e = (int)(t & kIdxMask);
-          int kin = K - 1 - d.edelta[e];
-          if (kin >= 0) em.put(varF(d, s, e, kin), false);
-        }
-        if (pair >= 0) em.put(varRd(d, pair, K - 1), true);
-      }
-      rlo = rhi = 0.0;
-    } else if (r < d.R_bcap) {                       // cum(p,k), lp.py:118-123
-      int64_t q = r - d.R_cum;
-      int p = (int)(q / K), k = (int)(q % K);
-      int64_t rd = varRd(d, p, k);
-      if (k >= 1) em.put(rd - 1, true);              // Rc(p,k-1)
-      em.put(rd, true);                              // Rd(p,k)
-      em.put(rd + 1, false);                         // Rc(p,k)
-      rlo = rhi = 0.0;
-    } else {                                         // bcap(g,k), lp.py:125-131
-      int64_t q = r - d.R_bcap;
-      int g = (int)(q / (K + 1)), k = (int)(q % (K + 1));
-      for (int s = 0; s < d.S; ++s) em.put(varB(d, s, g, k), false);
-      rlo = -INFINITY;
-      rhi = d.blimit;
-      rc = 1 + d.nOU + d.nCap;
-    }
+    double rlo, rhi;
+    int rc;
+    gen_row(d, r, em, rlo, rhi, rc);
     if (FILL) {
       lo[r] = rlo;
       hi[r] = rhi;
@@ -186,66 +197,78 @@ __device__ __forceinline__ void sort_small(int64_t* a, bool* neg, int n) {
   }
 }
 
+// gen_col: the (<= 6) reference rows of reference column v, unsorted, with
+// its bounds, cost and bound class; returns the entry count.
+__device__ __forceinline__ int gen_col(const TeDev& d, int64_t v, int64_t* rows, bool* neg,
+                                       double& vlb, double& vub, double& cost, int& cc) {
+  const int K = d.K;
+  const int64_t fB = (int64_t)d.E * K;
+  int c = 0;
+  vlb = 0.0;
+  vub = INFINITY;
+  cost = 0.0;
+  cc = 0;                                          // bound class 0 = (0, inf, 0)
+  if (v < (int64_t)d.S * d.SB) {
+    int s = (int)(v / d.SB);
+    int64_t q = v % d.SB;
+    if (q < fB) {                                  // F(s,e,k)
+      int e = (int)(q / K), k = (int)(q % K);
+      int u = d.esrc[e], w = d.edst[e];
+      if (k == 0 && u == d.snode[s]) { rows[c] = s; neg[c++] = false; }
+      rows[c] = d.S + (int64_t)e * K + k; neg[c++] = false;
+      if (k >= 1) { rows[c] = rowCons(d, s, u, k - 1); neg[c++] = true; }
+      int t = k + d.edelta[e];
+      if (t <= K - 1) { rows[c] = rowCons(d, s, w, t); neg[c++] = false; }
+      if (t == K - 1 && !d.is_sw[w] && w != d.snode[s]) {
+        rows[c] = rowCons(d, s, w, K); neg[c++] = false;
+      }
+      if (k == 0 && u != d.snode[s]) { vub = 0.0; cc = 1; }   // lp.py:51-52
+    } else {                                       // B(s,g,k)
+      q -= fB;
+      int g = (int)(q / (K + 1)), k = (int)(q % (K + 1));
+      int n = d.node_of_gpu[g];
+      if (k == 0 && n == d.snode[s]) { rows[c] = s; neg[c++] = false; }
+      if (k >= 1) { rows[c] = rowCons(d, s, n, k - 1); neg[c++] = true; }
+      if (k <= K - 1) { rows[c] = rowCons(d, s, n, k); neg[c++] = false; }
+      if (d.has_bcap) { rows[c] = d.R_bcap + (int64_t)g * (K + 1) + k; neg[c++] = false; }
+      if (k == 0 && n != d.snode[s]) { vub = 0.0; cc = 1; }   // lp.py:57-59
+    }
+  } else {
+    int64_t q = v - (int64_t)d.S * d.SB;
+    int p = (int)(q / (2 * K));
+    int k = (int)((q % (2 * K)) >> 1);
+    bool is_rc = (q & 1) != 0;
+    int s = d.pair_src[p], w = d.pair_dst[p];
+    double u = d.pair_u[p];
+    vub = u;
+    if (!is_rc) {                                  // Rd(p,k)
+      if (d.dict_col) cc = 2 + d.pair_uidx[p];
+      rows[c] = rowCons(d, s, w, k); neg[c++] = true;
+      if (k == K - 1) { rows[c] = rowCons(d, s, w, K); neg[c++] = true; }
+      rows[c] = d.R_cum + (int64_t)p * K + k; neg[c++] = true;
+    } else {                                       // Rc(p,k)
+      rows[c] = d.R_cum + (int64_t)p * K + k; neg[c++] = false;
+      if (k + 1 <= K - 1) { rows[c] = d.R_cum + (int64_t)p * K + k + 1; neg[c++] = true; }
+      if (k == K - 1) vlb = u;                     // lp.py:64-65
+      cost = -1.0 / (double)(k + 1);               // maximise sum Rc/(k+1), lp.py:133-135
+      if (d.dict_col) cc = 2 + d.nU + d.pair_uidx[p] * K + k;
+    }
+  }
+  return c;
+}
+
 template <bool FILL>
 __global__ void te_cols_kernel(TeDev d, const int64_t* __restrict__ col_ptr,
                                uint32_t* __restrict__ row, int64_t* __restrict__ col_len,
                                double* __restrict__ lb, double* __restrict__ ub,
                                double* __restrict__ obj, uint16_t* __restrict__ code) {
-  const int K = d.K;
-  const int64_t fB = (int64_t)d.E * K;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < d.n_vars;
        v += (int64_t)gridDim.x * blockDim.x) {
     int64_t rows[6];
     bool neg[6];
-    int c = 0;
-    double vlb = 0.0, vub = INFINITY, cost = 0.0;
-    int cc = 0;                                      // bound class 0 = (0, inf, 0)
-    if (v < (int64_t)d.S * d.SB) {
-      int s = (int)(v / d.SB);
-      int64_t q = v % d.SB;
-      if (q < fB) {                                  // F(s,e,k)
-        int e = (int)(q / K), k = (int)(q % K);
-        int u = d.esrc[e], w = d.edst[e];
-        if (k == 0 && u == d.snode[s]) { rows[c] = s; neg[c++] = false; }
-        rows[c] = d.S + (int64_t)e * K + k; neg[c++] = false;
-        if (k >= 1) { rows[c] = rowCons(d, s, u, k - 1); neg[c++] = true; }
-        int t = k + d.edelta[e];
-        if (t <= K - 1) { rows[c] = rowCons(d, s, w, t); neg[c++] = false; }
-        if (t == K - 1 && !d.is_sw[w] && w != d.snode[s]) {
-          rows[c] = rowCons(d, s, w, K); neg[c++] = false;
-        }
-        if (k == 0 && u != d.snode[s]) { vub = 0.0; cc = 1; }   // lp.py:51-52
-      } else {                                       // B(s,g,k)
-        q -= fB;
-        int g = (int)(q / (K + 1)), k = (int)(q % (K + 1));
-        int n = d.node_of_gpu[g];
-        if (k == 0 && n == d.snode[s]) { rows[c] = s; neg[c++] = false; }
-        if (k >= 1) { rows[c] = rowCons(d, s, n, k - 1); neg[c++] = true; }
-        if (k <= K - 1) { rows[c] = rowCons(d, s, n, k); neg[c++] = false; }
-        if (d.has_bcap) { rows[c] = d.R_bcap + (int64_t)g * (K + 1) + k; neg[c++] = false; }
-        if (k == 0 && n != d.snode[s]) { vub = 0.0; cc = 1; }   // lp.py:57-59
-      }
-    } else {
-      int64_t q = v - (int64_t)d.S * d.SB;
-      int p = (int)(q / (2 * K));
-      int k = (int)((q % (2 * K)) >> 1);
-      bool is_rc = (q & 1) != 0;
-      int s = d.pair_src[p], w = d.pair_dst[p];
-      double u = d.pair_u[p];
-      vub = u;
-      if (!is_rc) {                                  // Rd(p,k)
-        if (d.dict_col) cc = 2 + d.pair_uidx[p];
-        rows[c] = rowCons(d, s, w, k); neg[c++] = true;
-        if (k == K - 1) { rows[c] = rowCons(d, s, w, K); neg[c++] = true; }
-        rows[c] = d.R_cum + (int64_t)p * K + k; neg[c++] = true;
-      } else {                                       // Rc(p,k)
-        rows[c] = d.R_cum + (int64_t)p * K + k; neg[c++] = false;
-        if (k + 1 <= K - 1) { rows[c] = d.R_cum + (int64_t)p * K + k + 1; neg[c++] = true; }
-        if (k == K - 1) vlb = u;                     // lp.py:64-65
-        cost = -1.0 / (double)(k + 1);               // maximise sum Rc/(k+1), lp.py:133-135
-        if (d.dict_col) cc = 2 + d.nU + d.pair_uidx[p] * K + k;
-      }
-    }
+    double vlb, vub, cost;
+    int cc;
+    const int c = gen_col(d, v, rows, neg, vlb, vub, cost, cc);
     if (FILL) {
       sort_small(rows, neg, c);
       uint32_t* out = row + col_ptr[v];
@@ -263,6 +286,206 @@ __global__ void te_cols_kernel(TeDev d, const int64_t* __restrict__ col_ptr,
 __global__ void set_tail_kernel(int64_t* ptr, int64_t idx, const int64_t* len_last,
                                 const int64_t* scan_last) {
   ptr[idx] = *scan_last + *len_last;
+}
+
+// ---------------------------------------------------------------------------
+// Epoch-major numbering for row-partitioned (multi-GPU) solves. Columns:
+// epoch blocks of CW = S*E + S*G + 2P [F(s,e,k) | B(s,g,k) | Rd/Rc(p,k)], then
+// the S*G final buffers B(s,g,K). Rows: S init rows, epoch blocks of
+// RW = E + S*Nn + P (+G) [cap(e,k) | cons(s,n,k) | cum(p,k) | bcap(g,k)],
+// then the S*(G-1) last-epoch rows and bcap(g,K). Every row of epoch k only
+// touches columns of epochs k-delta_max..k+1, so contiguous epoch ranges give
+// contiguous owned ranges with thin contiguous halos.
+struct EmShape {
+  int64_t CW, RW, n_cols, n_rows;
+};
+
+__host__ __device__ inline EmShape em_shape(const TeDev& d) {
+  EmShape e;
+  e.CW = (int64_t)d.S * d.E + (int64_t)d.S * d.G + 2LL * d.P;
+  e.RW = (int64_t)d.E + (int64_t)d.S * d.Nn + d.P + (d.has_bcap ? d.G : 0);
+  e.n_cols = (int64_t)d.K * e.CW + (int64_t)d.S * d.G;
+  e.n_rows = d.S + (int64_t)d.K * e.RW + (int64_t)d.S * (d.G - 1) + (d.has_bcap ? d.G : 0);
+  return e;
+}
+
+__device__ inline int64_t em_col_of_ref(const TeDev& d, const EmShape& z, int64_t v) {
+  const int K = d.K;
+  if (v < (int64_t)d.S * d.SB) {
+    const int s = (int)(v / d.SB);
+    int64_t q = v % d.SB;
+    if (q < (int64_t)d.E * K) {
+      const int e = (int)(q / K), k = (int)(q % K);
+      return k * z.CW + (int64_t)s * d.E + e;
+    }
+    q -= (int64_t)d.E * K;
+    const int g = (int)(q / (K + 1)), k = (int)(q % (K + 1));
+    if (k < K) return k * z.CW + (int64_t)d.S * d.E + (int64_t)s * d.G + g;
+    return (int64_t)K * z.CW + (int64_t)s * d.G + g;
+  }
+  const int64_t q = v - (int64_t)d.S * d.SB;
+  const int p = (int)(q / (2 * K));
+  const int k = (int)((q % (2 * K)) >> 1);
+  return k * z.CW + (int64_t)d.S * d.E + (int64_t)d.S * d.G + 2LL * p + (q & 1);
+}
+
+__device__ inline int64_t ref_col_of_em(const TeDev& d, const EmShape& z, int64_t c) {
+  const int K = d.K;
+  int64_t k = c / z.CW;
+  if (k >= K) {
+    const int64_t o = c - (int64_t)K * z.CW;
+    return varB(d, (int)(o / d.G), (int)(o % d.G), K);
+  }
+  int64_t o = c - k * z.CW;
+  if (o < (int64_t)d.S * d.E) return varF(d, (int)(o / d.E), (int)(o % d.E), (int)k);
+  o -= (int64_t)d.S * d.E;
+  if (o < (int64_t)d.S * d.G) return varB(d, (int)(o / d.G), (int)(o % d.G), (int)k);
+  o -= (int64_t)d.S * d.G;
+  return varRd(d, (int)(o >> 1), (int)k) + (o & 1);
+}
+
+__device__ inline int node_of_cons(const TeDev& d, int s, int64_t off) {
+  int lo_n = 0, hi_n = d.Nn - 1;
+  while (lo_n < hi_n) {
+    const int mid = (lo_n + hi_n + 1) >> 1;
+    if (cons_off(d, s, mid) <= off) lo_n = mid; else hi_n = mid - 1;
+  }
+  return lo_n;
+}
+
+__device__ inline int64_t ref_row_of_em(const TeDev& d, const EmShape& z, int64_t r) {
+  const int K = d.K;
+  if (r < d.S) return r;
+  r -= d.S;
+  int64_t k = r / z.RW;
+  if (k >= K) {
+    int64_t o = r - (int64_t)K * z.RW;
+    if (o < (int64_t)d.S * (d.G - 1)) {
+      const int s = (int)(o / (d.G - 1)), i = (int)(o % (d.G - 1));
+      const int gs = d.gpu_of[d.snode[s]];
+      return rowCons(d, s, d.node_of_gpu[i < gs ? i : i + 1], K);
+    }
+    o -= (int64_t)d.S * (d.G - 1);
+    return d.R_bcap + o * (K + 1) + K;
+  }
+  int64_t o = r - k * z.RW;
+  if (o < d.E) return d.S + o * K + k;
+  o -= d.E;
+  if (o < (int64_t)d.S * d.Nn) return rowCons(d, (int)(o / d.Nn), (int)(o % d.Nn), (int)k);
+  o -= (int64_t)d.S * d.Nn;
+  if (o < d.P) return d.R_cum + o * K + k;
+  o -= d.P;
+  return d.R_bcap + o * (K + 1) + k;
+}
+
+__device__ inline int64_t em_row_of_ref(const TeDev& d, const EmShape& z, int64_t r) {
+  const int K = d.K;
+  if (r < d.S) return r;
+  if (r < d.R_cons) {
+    const int64_t q = r - d.S;
+    return d.S + (q % K) * z.RW + q / K;
+  }
+  if (r < d.R_cum) {
+    const int64_t q = r - d.R_cons;
+    const int s = (int)(q / d.CB);
+    const int64_t off = q % d.CB;
+    const int n = node_of_cons(d, s, off);
+    const int64_t k = off - cons_off(d, s, n);
+    if (k < K) return d.S + k * z.RW + d.E + (int64_t)s * d.Nn + n;
+    const int g = d.gpu_of[n], gs = d.gpu_of[d.snode[s]];
+    return d.S + (int64_t)K * z.RW + (int64_t)s * (d.G - 1) + (g < gs ? g : g - 1);
+  }
+  if (r < d.R_bcap) {
+    const int64_t q = r - d.R_cum;
+    return d.S + (q % K) * z.RW + d.E + (int64_t)d.S * d.Nn + q / K;
+  }
+  const int64_t q = r - d.R_bcap;
+  const int64_t g = q / (K + 1), k = q % (K + 1);
+  if (k < K) return d.S + k * z.RW + d.E + (int64_t)d.S * d.Nn + d.P + g;
+  return d.S + (int64_t)K * z.RW + (int64_t)d.S * (d.G - 1) + g;
+}
+
+// Emitter that maps reference columns to window-relative epoch-major ids.
+template <bool FILL>
+struct EmColEmitter {
+  const TeDev* d;
+  const EmShape* z;
+  uint32_t* out;
+  int64_t base;
+  int cnt;
+  unsigned long long* lo;
+  unsigned long long* hi;
+  __device__ __forceinline__ void put(int64_t v, bool neg) {
+    const int64_t c = em_col_of_ref(*d, *z, v);
+    if (FILL) out[cnt] = (uint32_t)(c - base) | (neg ? kSignBit : 0u);
+    else { atomicMin(lo, (unsigned long long)c); atomicMax(hi, (unsigned long long)c); }
+    ++cnt;
+  }
+};
+
+// Local rows [r0, r0+nr) of the epoch-major LP: CSR over the column window.
+template <bool FILL>
+__global__ void part_rows_kernel(TeDev d, EmShape z, int64_t r0, int64_t nr, int64_t cw0,
+                                 const int64_t* __restrict__ row_ptr, uint32_t* __restrict__ col,
+                                 int64_t* __restrict__ row_len, double* __restrict__ lo,
+                                 double* __restrict__ hi, uint16_t* __restrict__ code,
+                                 unsigned long long* mm) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nr;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = ref_row_of_em(d, z, r0 + i);
+    EmColEmitter<FILL> em{&d, &z, FILL ? col + row_ptr[i] : nullptr, cw0, 0, mm, mm + 1};
+    double rlo, rhi;
+    int rc;
+    gen_row(d, r, em, rlo, rhi, rc);
+    if (FILL) {
+      lo[i] = rlo;
+      hi[i] = rhi;
+      if (d.dict_row) code[i] = (uint16_t)rc;
+    } else {
+      row_len[i] = em.cnt;
+    }
+  }
+}
+
+// Local columns [c0, c0+nc): CSC over the row window.
+template <bool FILL>
+__global__ void part_cols_kernel(TeDev d, EmShape z, int64_t c0, int64_t nc, int64_t rw0,
+                                 const int64_t* __restrict__ col_ptr, uint32_t* __restrict__ row,
+                                 int64_t* __restrict__ col_len, double* __restrict__ lb,
+                                 double* __restrict__ ub, double* __restrict__ obj,
+                                 uint16_t* __restrict__ code, unsigned long long* mm) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nc;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = ref_col_of_em(d, z, c0 + j);
+    int64_t rows[6];
+    bool neg[6];
+    double vlb, vub, cost;
+    int cc;
+    const int c = gen_col(d, v, rows, neg, vlb, vub, cost, cc);
+    for (int q = 0; q < c; ++q) rows[q] = em_row_of_ref(d, z, rows[q]);
+    if (FILL) {
+      sort_small(rows, neg, c);
+      uint32_t* out = row + col_ptr[j];
+      for (int q = 0; q < c; ++q) out[q] = (uint32_t)(rows[q] - rw0) | (neg[q] ? kSignBit : 0u);
+      lb[j] = vlb;
+      ub[j] = vub;
+      obj[j] = cost;
+      if (d.dict_col) code[j] = (uint16_t)cc;
+    } else {
+      col_len[j] = c;
+      for (int q = 0; q < c; ++q) {
+        atomicMin(mm, (unsigned long long)rows[q]);
+        atomicMax(mm + 1, (unsigned long long)rows[q]);
+      }
+    }
+  }
+}
+
+// ref index of every local (epoch-major) column: host assembles solutions
+__global__ void part_colmap_kernel(TeDev d, EmShape z, int64_t c0, int64_t nc, int64_t* out) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nc;
+       j += (int64_t)gridDim.x * blockDim.x)
+    out[j] = ref_col_of_em(d, z, c0 + j);
 }
 
 }  // namespace teccl
@@ -395,35 +618,14 @@ int prepare_tables(teccl_ctx* ctx, const teccl_te_desc* desc, TeDev& d, std::vec
 
 }  // namespace
 
-extern "C" int teccl_lp_build_te(teccl_ctx* ctx, const teccl_te_desc* desc, teccl_lp** out) {
-  if (!ctx || !desc || !out) { set_error("null argument"); return TECCL_EINVAL; }
-  TeDev d;
-  std::vector<void*> owned;
-  cudaStream_t st = ctx->stream;
-  int prc = prepare_tables(ctx, desc, d, owned);
-  if (prc) { for (void* p : owned) cudaFreeAsync(p, st); return prc; }
-  teccl_lp* lp = new teccl_lp();
-  lp->m = (int32_t)d.n_rows;
-  lp->n = (int32_t)d.n_vars;
-  lp->unit = true;
-  lp->device = ctx->device;
-  lp->stream = st;
-  const int64_t m = d.n_rows, n = d.n_vars;
-  int64_t *row_len = nullptr, *col_len = nullptr;
-  TECCL_CUDA(cudaMallocAsync((void**)&lp->row_ptr, (m + 1) * sizeof(int64_t), st));
-  TECCL_CUDA(cudaMallocAsync((void**)&lp->col_ptr, (n + 1) * sizeof(int64_t), st));
-  TECCL_CUDA(cudaMallocAsync((void**)&row_len, (m + 1) * sizeof(int64_t), st));
-  TECCL_CUDA(cudaMallocAsync((void**)&col_len, (n + 1) * sizeof(int64_t), st));
-  TECCL_CUDA(cudaMallocAsync((void**)&lp->row_lo, (m + 1) * sizeof(double), st));
-  TECCL_CUDA(cudaMallocAsync((void**)&lp->row_hi, (m + 1) * sizeof(double), st));
-  TECCL_CUDA(cudaMallocAsync((void**)&lp->var_lb, (n + 1) * sizeof(double), st));
-  TECCL_CUDA(cudaMallocAsync((void**)&lp->var_ub, (n + 1) * sizeof(double), st));
-  TECCL_CUDA(cudaMallocAsync((void**)&lp->obj, (n + 1) * sizeof(double), st));
+namespace {
 
-  // Bound-class dictionaries (pdlp.cu reads bounds/costs through them).
-  // Columns: [0] free (0,inf,0), [1] fixed (0,0,0), [2+u] Rd (0,U_u,0),
-  // [2+nU+u*K+k] Rc (0 or U_u at k=K-1, U_u, -1/(k+1)). Rows: [0] (0,0),
-  // [1+o] init (OU_o,OU_o), [1+nOU+c] cap (-inf,CAP_c), [1+nOU+nCap] bcap.
+// Bound-class dictionaries (pdlp.cu reads bounds/costs through them).
+// Columns: [0] free (0,inf,0), [1] fixed (0,0,0), [2+u] Rd (0,U_u,0),
+// [2+nU+u*K+k] Rc (0 or U_u at k=K-1, U_u, -1/(k+1)). Rows: [0] (0,0),
+// [1+o] init (OU_o,OU_o), [1+nOU+c] cap (-inf,CAP_c), [1+nOU+nCap] bcap.
+int setup_dicts(const teccl_te_desc* desc, TeDev& d, teccl_lp* lp, std::vector<void*>& owned,
+                cudaStream_t st, int64_t m, int64_t n) {
   {
     std::vector<double> U(desc->pair_units, desc->pair_units + desc->num_pairs);
     std::sort(U.begin(), U.end());
@@ -488,6 +690,37 @@ extern "C" int teccl_lp_build_te(teccl_ctx* ctx, const teccl_te_desc* desc, tecc
       TECCL_CUDA(cudaMallocAsync((void**)&lp->row_code, (m + 1) * sizeof(uint16_t), st));
     }
   }
+  return TECCL_OK;
+}
+
+}  // namespace
+
+extern "C" int teccl_lp_build_te(teccl_ctx* ctx, const teccl_te_desc* desc, teccl_lp** out) {
+  if (!ctx || !desc || !out) { set_error("null argument"); return TECCL_EINVAL; }
+  TeDev d;
+  std::vector<void*> owned;
+  cudaStream_t st = ctx->stream;
+  int prc = prepare_tables(ctx, desc, d, owned);
+  if (prc) { for (void* p : owned) cudaFreeAsync(p, st); return prc; }
+  teccl_lp* lp = new teccl_lp();
+  lp->m = (int32_t)d.n_rows;
+  lp->n = (int32_t)d.n_vars;
+  lp->unit = true;
+  lp->device = ctx->device;
+  lp->stream = st;
+  const int64_t m = d.n_rows, n = d.n_vars;
+  int64_t *row_len = nullptr, *col_len = nullptr;
+  TECCL_CUDA(cudaMallocAsync((void**)&lp->row_ptr, (m + 1) * sizeof(int64_t), st));
+  TECCL_CUDA(cudaMallocAsync((void**)&lp->col_ptr, (n + 1) * sizeof(int64_t), st));
+  TECCL_CUDA(cudaMallocAsync((void**)&row_len, (m + 1) * sizeof(int64_t), st));
+  TECCL_CUDA(cudaMallocAsync((void**)&col_len, (n + 1) * sizeof(int64_t), st));
+  TECCL_CUDA(cudaMallocAsync((void**)&lp->row_lo, (m + 1) * sizeof(double), st));
+  TECCL_CUDA(cudaMallocAsync((void**)&lp->row_hi, (m + 1) * sizeof(double), st));
+  TECCL_CUDA(cudaMallocAsync((void**)&lp->var_lb, (n + 1) * sizeof(double), st));
+  TECCL_CUDA(cudaMallocAsync((void**)&lp->var_ub, (n + 1) * sizeof(double), st));
+  TECCL_CUDA(cudaMallocAsync((void**)&lp->obj, (n + 1) * sizeof(double), st));
+
+  if (int rc = setup_dicts(desc, d, lp, owned, st, m, n)) return rc;
 
   if (m > 0) {
     te_rows_kernel<false><<<grid_for(m), kThreads, 0, st>>>(d, nullptr, nullptr, row_len, nullptr, nullptr, nullptr);
@@ -526,6 +759,123 @@ extern "C" int teccl_lp_build_te(teccl_ctx* ctx, const teccl_te_desc* desc, tecc
   TECCL_CUDA(cudaFreeAsync(col_len, st));
   for (void* p : owned) TECCL_CUDA(cudaFreeAsync(p, st));
   TECCL_CUDA(cudaStreamSynchronize(st));
+  *out = lp;
+  return TECCL_OK;
+}
+
+
+extern "C" int teccl_lp_build_te_part(teccl_ctx* ctx, const teccl_te_desc* desc, int32_t world,
+                                      int32_t rank, teccl_lp** out, int64_t* info) {
+  if (!ctx || !desc || !out || !info) { set_error("null argument"); return TECCL_EINVAL; }
+  if (world < 1 || rank < 0 || rank >= world) { set_error("bad world/rank"); return TECCL_EINVAL; }
+  TeDev d;
+  std::vector<void*> owned;
+  cudaStream_t st = ctx->stream;
+  int prc = prepare_tables(ctx, desc, d, owned);
+  if (prc) { for (void* p : owned) cudaFreeAsync(p, st); return prc; }
+  const EmShape z = em_shape(d);
+  const int K = d.K;
+  int dmax = 0;
+  for (int e = 0; e < desc->num_edges; ++e) dmax = std::max(dmax, (int)desc->edge_delta[e]);
+  auto krange = [&](int r, int64_t& k0, int64_t& k1) {
+    k0 = (int64_t)r * K / world;
+    k1 = (int64_t)(r + 1) * K / world;
+  };
+  auto owned_cols = [&](int r, int64_t& c0, int64_t& c1) {
+    int64_t k0, k1;
+    krange(r, k0, k1);
+    c0 = k0 * z.CW;
+    c1 = (r == world - 1) ? z.n_cols : k1 * z.CW;
+  };
+  auto owned_rows = [&](int r, int64_t& r0, int64_t& r1) {
+    int64_t k0, k1;
+    krange(r, k0, k1);
+    r0 = (r == 0) ? 0 : d.S + k0 * z.RW;
+    r1 = (r == world - 1) ? z.n_rows : d.S + k1 * z.RW;
+  };
+  for (int r = 0; r < world; ++r) {
+    int64_t k0, k1;
+    krange(r, k0, k1);
+    if (world > 1 && k1 - k0 < dmax + 2) {
+      set_error("epoch blocks too thin: every rank needs >= delta_max + 2 epochs");
+      return TECCL_EINVAL;
+    }
+  }
+  int64_t k0, k1, c0, c1, r0, r1;
+  krange(rank, k0, k1);
+  owned_cols(rank, c0, c1);
+  owned_rows(rank, r0, r1);
+  const int64_t nr = r1 - r0, nc = c1 - c0;
+  if (nr >= (int64_t)kSignBit || nc >= (int64_t)kSignBit) {
+    set_error("partition too large for 31-bit local indices; use more ranks");
+    return TECCL_EINVAL;
+  }
+  teccl_lp* lp = new teccl_lp();
+  lp->m = (int32_t)nr;
+  lp->n = (int32_t)nc;
+  lp->unit = true;
+  lp->device = ctx->device;
+  lp->stream = st;
+  lp->part_world = world;
+  lp->part_rank = rank;
+  lp->em_ncols = z.n_cols;
+  lp->em_nrows = z.n_rows;
+  lp->own_c0 = c0; lp->own_c1 = c1; lp->own_r0 = r0; lp->own_r1 = r1;
+  int64_t *row_len = nullptr, *col_len = nullptr;
+  unsigned long long* mm = nullptr;
+  TECCL_CUDA(cudaMallocAsync((void**)&lp->row_ptr, (nr + 1) * sizeof(int64_t), st));
+  TECCL_CUDA(cudaMallocAsync((void**)&lp->col_ptr, (nc + 1) * sizeof(int64_t), st));
+  TECCL_CUDA(cudaMallocAsync((void**)&row_len, (nr + 1) * sizeof(int64_t), st));
+  TECCL_CUDA(cudaMallocAsync((void**)&col_len, (nc + 1) * sizeof(int64_t), st));
+  TECCL_CUDA(cudaMallocAsync((void**)&lp->row_lo, (nr + 1) * sizeof(double), st));
+  TECCL_CUDA(cudaMallocAsync((void**)&lp->row_hi, (nr + 1) * sizeof(double), st));
+  TECCL_CUDA(cudaMallocAsync((void**)&lp->var_lb, (nc + 1) * sizeof(double), st));
+  TECCL_CUDA(cudaMallocAsync((void**)&lp->var_ub, (nc + 1) * sizeof(double), st));
+  TECCL_CUDA(cudaMallocAsync((void**)&lp->obj, (nc + 1) * sizeof(double), st));
+  TECCL_CUDA(cudaMallocAsync((void**)&mm, 4 * sizeof(unsigned long long), st));
+  const unsigned long long mm0[4] = {~0ull, 0ull, ~0ull, 0ull};
+  TECCL_CUDA(cudaMemcpyAsync(mm, mm0, sizeof(mm0), cudaMemcpyHostToDevice, st));
+  if (int rc = setup_dicts(desc, d, lp, owned, st, nr, nc)) return rc;
+
+  part_rows_kernel<false><<<grid_for(nr), kThreads, 0, st>>>(d, z, r0, nr, 0, nullptr, nullptr, row_len, nullptr, nullptr, nullptr, mm);
+  part_cols_kernel<false><<<grid_for(nc), kThreads, 0, st>>>(d, z, c0, nc, 0, nullptr, nullptr, col_len, nullptr, nullptr, nullptr, nullptr, mm + 2);
+  TECCL_CHECK_LAUNCH();
+  if (scan_lengths(row_len, lp->row_ptr, nr, st)) return TECCL_ECUDA;
+  if (scan_lengths(col_len, lp->col_ptr, nc, st)) return TECCL_ECUDA;
+  unsigned long long mmh[4];
+  int64_t nnz_r = 0, nnz_c = 0;
+  TECCL_CUDA(cudaMemcpyAsync(mmh, mm, sizeof(mmh), cudaMemcpyDeviceToHost, st));
+  TECCL_CUDA(cudaMemcpyAsync(&nnz_r, lp->row_ptr + nr, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  TECCL_CUDA(cudaMemcpyAsync(&nnz_c, lp->col_ptr + nc, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  TECCL_CUDA(cudaStreamSynchronize(st));
+  const int64_t cw0 = std::min<int64_t>(nnz_r ? (int64_t)mmh[0] : c0, c0);
+  const int64_t cw1 = std::max<int64_t>(nnz_r ? (int64_t)mmh[1] + 1 : c1, c1);
+  const int64_t rw0 = std::min<int64_t>(nnz_c ? (int64_t)mmh[2] : r0, r0);
+  const int64_t rw1 = std::max<int64_t>(nnz_c ? (int64_t)mmh[3] + 1 : r1, r1);
+  // halos must come from the two neighbours only
+  if (world > 1) {
+    int64_t a, b;
+    if (rank > 0) { owned_cols(rank - 1, a, b); if (cw0 < a) { set_error("column halo reaches past the previous rank"); return TECCL_EINVAL; } }
+    if (rank < world - 1) { owned_cols(rank + 1, a, b); if (cw1 > b) { set_error("column halo reaches past the next rank"); return TECCL_EINVAL; } }
+    if (rank > 0) { owned_rows(rank - 1, a, b); if (rw0 < a) { set_error("row halo reaches past the previous rank"); return TECCL_EINVAL; } }
+    if (rank < world - 1) { owned_rows(rank + 1, a, b); if (rw1 > b) { set_error("row halo reaches past the next rank"); return TECCL_EINVAL; } }
+  }
+  lp->win_c0 = cw0; lp->win_c1 = cw1; lp->win_r0 = rw0; lp->win_r1 = rw1;
+  lp->nnz = nnz_r;
+  lp->nnz_csc = nnz_c;
+  TECCL_CUDA(cudaMallocAsync((void**)&lp->col, (nnz_r + 1) * sizeof(uint32_t), st));
+  TECCL_CUDA(cudaMallocAsync((void**)&lp->row, (nnz_c + 1) * sizeof(uint32_t), st));
+  part_rows_kernel<true><<<grid_for(nr), kThreads, 0, st>>>(d, z, r0, nr, cw0, lp->row_ptr, lp->col, nullptr, lp->row_lo, lp->row_hi, lp->row_code, mm);
+  part_cols_kernel<true><<<grid_for(nc), kThreads, 0, st>>>(d, z, c0, nc, rw0, lp->col_ptr, lp->row, nullptr, lp->var_lb, lp->var_ub, lp->obj, lp->col_code, mm + 2);
+  TECCL_CHECK_LAUNCH();
+  TECCL_CUDA(cudaFreeAsync(row_len, st));
+  TECCL_CUDA(cudaFreeAsync(col_len, st));
+  TECCL_CUDA(cudaFreeAsync(mm, st));
+  for (void* p : owned) TECCL_CUDA(cudaFreeAsync(p, st));
+  TECCL_CUDA(cudaStreamSynchronize(st));
+  const int64_t vals[16] = {c0, c1, r0, r1, cw0, cw1, rw0, rw1, k0, k1, z.n_cols, z.n_rows,
+                            dmax, nnz_r, nnz_c, z.CW};
+  for (int i = 0; i < 16; ++i) info[i] = vals[i];
   *out = lp;
   return TECCL_OK;
 }
