@@ -117,6 +117,25 @@ def solve_partitioned(t, d, cfg, opts=None, eps_rel: float = 1e-4, max_iters: in
     if device is None:
         device = torch.cuda.current_device()
     plan = make_plan(t, d, cfg, opts)
+    if world == 1:  # nothing to partition: the single-device path
+        from .lp import build_from_plan
+        from .solver import solve
+        lp = build_from_plan(plan, device)
+        sol = solve(lp, SolverOptions(eps_rel=eps_rel, max_iters=max_iters, device=device,
+                                      pdlp=pdlp or {}))
+        out = {"status": sol.status, "objective": sol.objective, "iters": sol.meta["iters"],
+               "restarts": sol.meta["restarts"], "rel_gap": sol.meta["rel_gap"],
+               "rel_primal_res": sol.meta["rel_primal_res"],
+               "rel_dual_res": sol.meta["rel_dual_res"],
+               "device_seconds": sol.meta["device_seconds"],
+               "kernel_launches": sol.meta["kernel_launches"], "world": 1, "rank": 0,
+               "info": {"own_c0": 0, "own_c1": plan.num_vars, "k0": 0, "k1": plan.K,
+                        "total_cols": plan.num_vars, "total_rows": plan.num_rows}}
+        if gather:
+            out["x"] = sol.x
+            out["plan"] = plan
+        lp.close()
+        return out
     part = build_partition(plan, world, rank, device)
     blobs = [None] * world
     dist.all_gather_object(blobs, export_blob(part), group=group)
