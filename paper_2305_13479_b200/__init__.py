@@ -12,6 +12,7 @@ from .epochs import EpochConfig, compute_delta, epoch_duration
 from .errors import (CollschedError, ConservationError, HorizonInfeasibleError,
                      ScheduleError, SolverBackendError, SolverTimeoutError, ValidationError)
 from .lp import DeviceLP, LpPlan, ModelOptions, build_lp_model, lp_completion_epoch, make_plan
+from .schedule import Schedule, ScheduleEvent, lp_rates_to_schedule
 from .solver import Solution, SolverOptions, min_feasible_horizon, solve
 from .topology import Edge, Topology, validate_topology
 
@@ -21,5 +22,6 @@ __all__ = [
     "HorizonInfeasibleError", "ScheduleError", "SolverBackendError", "SolverTimeoutError",
     "ValidationError", "DeviceLP", "LpPlan", "ModelOptions", "build_lp_model",
     "lp_completion_epoch", "make_plan", "Solution", "SolverOptions", "min_feasible_horizon",
-    "solve", "Edge", "Topology", "validate_topology",
+    "solve", "Edge", "Topology", "validate_topology", "Schedule", "ScheduleEvent",
+    "lp_rates_to_schedule",
 ]

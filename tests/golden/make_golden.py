@@ -23,7 +23,7 @@ import collsched.demand as rdem  # noqa: E402
 import collsched.epochs as rep  # noqa: E402
 import collsched.topology as rtopo  # noqa: E402
 from collsched.epochs import EpochConfig  # noqa: E402
-from collsched.lp import build_lp_model, lp_completion_epoch  # noqa: E402
+from collsched.lp import build_lp_model, lp_completion_epoch, lp_rates_to_schedule  # noqa: E402
 from collsched.milp import ModelOptions  # noqa: E402
 from collsched.model import INF  # noqa: E402
 from collsched.solver import SolverOptions, solve  # noqa: E402
@@ -77,6 +77,9 @@ def main():
         if sol.feasible:
             entry["completion_epoch"] = lp_completion_epoch(sol)
             x = np.asarray(sol.x)
+            sched = lp_rates_to_schedule(sol, t_ref, d_ref, cfg)
+            entry["schedule"] = [[e.source, e.chunk, e.src, e.dst, e.epoch, e.fraction]
+                                 for e in sched.events]
         np.savez_compressed(os.path.join(HERE, f"{name}.npz"), x=x, **arrays)
         summary[name] = entry
         print(name, entry, flush=True)
