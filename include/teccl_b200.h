@@ -76,6 +76,8 @@ typedef struct {
   const int32_t* pair_dst;        /* [P] node index */
   const double* pair_units;       /* [P] demanded chunks of the pair */
   double buffer_limit;            /* < 0: no Appendix-B buffer rows */
+  int32_t phase1;                 /* 1: feasibility LP -- maximise sum_p Rc(p,K-1) with
+                                     Rc(p,K-1) in [0,u] (feasible iff it reaches sum u) */
 } teccl_te_desc;
 
 int teccl_lp_build_te(teccl_ctx* ctx, const teccl_te_desc* desc, teccl_lp** out);

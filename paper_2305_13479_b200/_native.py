@@ -40,6 +40,7 @@ class TeDesc(C.Structure):
         ("edge_cap", _p(C.c_double)), ("source_node", _p(C.c_int32)),
         ("pair_source", _p(C.c_int32)), ("pair_dst", _p(C.c_int32)),
         ("pair_units", _p(C.c_double)), ("buffer_limit", C.c_double),
+        ("phase1", C.c_int32),
     ]
 
 

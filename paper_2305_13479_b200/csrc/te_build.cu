@@ -48,6 +48,7 @@ struct TeDev {
   const int* out_e;
   // bound-class codes (pdlp.cu dictionaries)
   int dict_col, dict_row, nU, nOU, nCap;
+  int phase1;
   const int* pair_uidx;  // [P] index of the pair's units in the distinct-units list
   const int* src_ouidx;  // [S] index of the source's out-units in its list
   const uint16_t* cap_idx;  // [E*K] index of the capacity in the distinct-caps list
@@ -249,8 +250,12 @@ __device__ __forceinline__ int gen_col(const TeDev& d, int64_t v, int64_t* rows,
     } else {                                       // Rc(p,k)
       rows[c] = d.R_cum + (int64_t)p * K + k; neg[c++] = false;
       if (k + 1 <= K - 1) { rows[c] = d.R_cum + (int64_t)p * K + k + 1; neg[c++] = true; }
-      if (k == K - 1) vlb = u;                     // lp.py:64-65
-      cost = -1.0 / (double)(k + 1);               // maximise sum Rc/(k+1), lp.py:133-135
+      if (d.phase1) {                              // feasibility: deliver everything by K-1
+        cost = (k == K - 1) ? -1.0 : 0.0;
+      } else {
+        if (k == K - 1) vlb = u;                   // lp.py:64-65
+        cost = -1.0 / (double)(k + 1);             // maximise sum Rc/(k+1), lp.py:133-135
+      }
       if (d.dict_col) cc = 2 + d.nU + d.pair_uidx[p] * K + k;
     }
   }
@@ -575,6 +580,7 @@ int prepare_tables(teccl_ctx* ctx, const teccl_te_desc* desc, TeDev& d, std::vec
   d.R_cum = d.R_cons + (int64_t)S * d.CB;
   d.R_bcap = d.R_cum + (int64_t)P * K;
   d.has_bcap = desc->buffer_limit >= 0.0;
+  d.phase1 = desc->phase1 != 0;
   d.blimit = desc->buffer_limit;
   d.n_rows = d.R_bcap + (d.has_bcap ? (int64_t)G * (K + 1) : 0);
   d.n_vars = (int64_t)S * d.SB + (int64_t)P * 2 * K;
@@ -649,7 +655,7 @@ int setup_dicts(const teccl_te_desc* desc, TeDev& d, teccl_lp* lp, std::vector<v
     const int64_t ncd = 2 + (int64_t)nU * (K + 1);
     const int64_t nrd = 1 + nOU + nCap + 1;
     d.nU = nU; d.nOU = nOU; d.nCap = nCap;
-    d.dict_col = ncd <= kMaxDict;
+    d.dict_col = ncd <= kMaxDict && !d.phase1;  // phase-1 costs are not in the dictionary
     d.dict_row = nrd <= kMaxDict;
     if (d.dict_col) {
       std::vector<double> cd(3 * ncd);

@@ -65,6 +65,7 @@ class LpPlan:
     pair_units: np.ndarray     # float64 [P]
     K: int
     buffer_limit: float
+    phase1: bool = False          # feasibility LP (see feasibility_gap)
     _desc: object = field(default=None, repr=False)
 
     @property
@@ -148,6 +149,7 @@ class LpPlan:
             d.pair_dst = nat.ptr(self.pair_dst, C.c_int32)
             d.pair_units = nat.ptr(self.pair_units, C.c_double)
             d.buffer_limit = float(self.buffer_limit)
+            d.phase1 = 1 if self.phase1 else 0
             self._desc = d
         return self._desc
 
@@ -283,3 +285,25 @@ def lp_completion_epoch(sol, tol: float = TOL) -> int:
         s, dst = plan.pairs[bad][0]
         raise ConservationError(f"pair ({s!r},{dst!r}) never reaches its demand")
     return int(ok.argmax(axis=1).max()) if plan.P else 0
+
+
+def feasibility_gap(plan: LpPlan, device: int = 0, eps_rel: float = 1e-7,
+                    max_iters: int = 2_000_000) -> float:
+    """Demand (in chunks) the horizon cannot deliver: solve the phase-1 LP --
+    same rows, final cumulative reads free in [0, u], maximise their sum --
+    and return sum(u) minus its optimum (0 up to solver accuracy iff the
+    reference's LP at this horizon is feasible)."""
+    from dataclasses import replace
+    from .solver import SolverOptions, solve
+    p1 = replace(plan, phase1=True, _desc=None)
+    lp = build_from_plan(p1, device)
+    sol = solve(lp, SolverOptions(eps_rel=eps_rel, max_iters=max_iters, device=device))
+    lp.close()
+    return float(plan.pair_units.sum() - sol.objective)
+
+
+def horizon_feasible(plan: LpPlan, device: int = 0) -> bool:
+    """Feasibility verdict for min_feasible_horizon: unmet demand above
+    max(1e-3 chunk, 1e-6 of the total) means infeasible."""
+    gap = feasibility_gap(plan, device)
+    return gap <= max(1e-3, 1e-6 * float(plan.pair_units.sum()))

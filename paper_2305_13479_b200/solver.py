@@ -155,14 +155,28 @@ def solve(m, opts: SolverOptions | None = None, relax_integrality: bool = False,
 
 def min_feasible_horizon(builder: Callable[[int], object], k_lo: int, k_hi: int,
                          opts: SolverOptions | None = None) -> tuple[int, Solution]:
-    """Binary search of the smallest feasible horizon (solver.py:140-169)."""
+    """Binary search of the smallest feasible horizon (solver.py:140-169).
+
+    A first-order method cannot certify infeasibility by itself; for models
+    from build_lp_model every probe first solves the phase-1 LP
+    (lp.feasibility_gap), exactly like the reference's HiGHS infeasible
+    status drives its search."""
     if k_lo < 1 or k_hi < k_lo:
         raise ValidationError(f"bad horizon range [{k_lo}, {k_hi}]")
+    from .lp import horizon_feasible
     best = None
     lo, hi = k_lo, k_hi
     while lo <= hi:
         mid = (lo + hi) // 2
-        sol = solve(builder(mid), opts)
+        m = builder(mid)
+        plan = getattr(m, "plan", None)
+        if plan is not None:
+            # time-expanded model: certify (in)feasibility with the phase-1 LP,
+            # then solve the real LP only at feasible horizons
+            ok = horizon_feasible(plan, getattr(m.ctx, "device", 0))
+            sol = solve(m, opts) if ok else Solution(INFEASIBLE, m)
+        else:
+            sol = solve(m, opts)
         if sol.feasible:
             best = (mid, sol)
             hi = mid - 1
