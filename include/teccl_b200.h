@@ -137,10 +137,13 @@ typedef struct {
   double reflection;       /* Halpern reflection coefficient in [0,1] (1.0) */
   int32_t use_graphs;      /* 1: replay each chunk from a CUDA graph */
   int32_t warm_start;      /* 1: start from x_inout / y_inout */
-  double restart_sufficient;  /* restart when r <= this * r0 (0.2) */
-  double restart_necessary;   /* ... or r <= this * r0 and r grew (0.8) */
+  double restart_sufficient;  /* restart when r <= this * r0 (0.3) */
+  double restart_necessary;   /* ... or r <= this * r0 and r grew (0.9) */
   double restart_artificial;  /* ... or inner iterations >= this * total (0.36) */
-  double omega_theta;         /* primal-weight smoothing at restarts, 0..1 (0.5) */
+  double omega_theta;         /* primal-weight proportional gain at restarts, 0..1 (0.7) */
+  double omega_scale;         /* multiplies the initial primal weight (1.0) */
+  double omega_ki;            /* integral gain of the primal-weight PID (0) */
+  double omega_kd;            /* derivative gain of the primal-weight PID (0) */
 } teccl_pdlp_opts;
 
 typedef struct {

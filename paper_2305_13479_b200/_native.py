@@ -51,7 +51,8 @@ class PdlpOpts(C.Structure):
         ("verbose", C.c_int32), ("reflection", C.c_double), ("use_graphs", C.c_int32),
         ("warm_start", C.c_int32), ("restart_sufficient", C.c_double),
         ("restart_necessary", C.c_double), ("restart_artificial", C.c_double),
-        ("omega_theta", C.c_double),
+        ("omega_theta", C.c_double), ("omega_scale", C.c_double),
+        ("omega_ki", C.c_double), ("omega_kd", C.c_double),
     ]
 
 

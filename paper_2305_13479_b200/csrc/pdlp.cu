@@ -54,7 +54,7 @@ struct PdlpState {
   double bnorm, cnorm;       // unscaled norms for the relative criteria
   double eps;
   double r0, rprev, last_r;
-  double rs_suff, rs_nec, rs_art, theta;
+  double rs_suff, rs_nec, rs_art, theta, ki, kd, e_int, e_prev;
   long long k_inner, total;
   int have_r0, restart, done, restarts, chunk_len, pad;
   double rel_p, rel_d, gap, pobj, dobj;
@@ -497,7 +497,13 @@ __global__ void control_kernel(Vecs V) {
     st->have_r0 = 0;
     const double dxr = sqrt(q[Q_DX0]), dyr = sqrt(q[Q_DY0]);
     if (dxr > 1e-10 && dyr > 1e-10) {
-      st->omega = exp(st->theta * log(dyr / dxr) + (1.0 - st->theta) * log(w));
+      // PID on the log primal-weight error e = log(dy/dx) - log(w); with
+      // ki = kd = 0 this is PDLP's exponential smoothing with weight theta
+      const double e = log(dyr / dxr) - log(w);
+      st->e_int += e;
+      const double de = e - st->e_prev;
+      st->e_prev = e;
+      st->omega = exp(log(w) + st->theta * e + st->ki * st->e_int + st->kd * de);
       st->tau = st->eta / st->omega;
       st->sigma = st->eta * st->omega;
     }
@@ -1089,7 +1095,7 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
   // --- state: omega in original space = scaled weight * gamma / beta
   PdlpState hs{};
   hs.eta = 0.998 / sigma_max;
-  hs.omega = omega_s * gamma / beta;
+  hs.omega = omega_s * gamma / beta * (o->omega_scale > 0.0 ? o->omega_scale : 1.0);
   hs.tau = hs.eta / hs.omega;
   hs.sigma = hs.eta * hs.omega;
   hs.refl = o->reflection;
@@ -1100,6 +1106,8 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
   hs.rs_nec = o->restart_necessary;
   hs.rs_art = o->restart_artificial;
   hs.theta = o->omega_theta;
+  hs.ki = o->omega_ki;
+  hs.kd = o->omega_kd;
   const int chunk = o->check_every > 0 ? o->check_every : 64;
   hs.chunk_len = chunk;
   TECCL_CUDA(cudaMemcpyAsync(dst, &hs, sizeof(hs), cudaMemcpyHostToDevice, st));
@@ -1297,10 +1305,13 @@ extern "C" void teccl_pdlp_default_opts(teccl_pdlp_opts* o) {
   o->reflection = 1.0;
   o->use_graphs = 1;
   o->warm_start = 0;
-  o->restart_sufficient = 0.2;
-  o->restart_necessary = 0.8;
+  o->restart_sufficient = 0.3;
+  o->restart_necessary = 0.9;
   o->restart_artificial = 0.36;
-  o->omega_theta = 0.5;
+  o->omega_theta = 0.7;
+  o->omega_scale = 1.0;
+  o->omega_ki = 0.0;
+  o->omega_kd = 0.0;
 }
 
 extern "C" int teccl_pdlp_solve_dev(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* opts,
