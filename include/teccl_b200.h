@@ -140,7 +140,7 @@ typedef struct {
   double restart_sufficient;  /* restart when r <= this * r0 (0.3) */
   double restart_necessary;   /* ... or r <= this * r0 and r grew (0.9) */
   double restart_artificial;  /* ... or inner iterations >= this * total (0.36) */
-  double omega_theta;         /* primal-weight proportional gain at restarts, 0..1 (0.7) */
+  double omega_theta;         /* primal-weight proportional gain at restarts, 0..1 (0.6) */
   double omega_scale;         /* multiplies the initial primal weight (1.0) */
   double omega_ki;            /* integral gain of the primal-weight PID (0) */
   double omega_kd;            /* derivative gain of the primal-weight PID (0) */

@@ -469,7 +469,8 @@ __global__ void control_kernel(Vecs V) {
   const double dobj = q[Q_DOBJ_ROW] + q[Q_DOBJ_COL];
   st->rel_p = sqrt(q[Q_RP]) / (1.0 + st->bnorm);
   st->rel_d = sqrt(q[Q_RD]) / (1.0 + st->cnorm);
-  st->gap = fabs(pobj - dobj) / (1.0 + fabs(pobj) + fabs(dobj));
+  // relative duality gap in the usual sense: |p - d| / max(1, |p|, |d|)
+  st->gap = fabs(pobj - dobj) / fmax(1.0, fmax(fabs(pobj), fabs(dobj)));
   st->pobj = pobj;
   st->dobj = dobj;
   st->last_r = r;
@@ -1308,7 +1309,7 @@ extern "C" void teccl_pdlp_default_opts(teccl_pdlp_opts* o) {
   o->restart_sufficient = 0.3;
   o->restart_necessary = 0.9;
   o->restart_artificial = 0.36;
-  o->omega_theta = 0.7;
+  o->omega_theta = 0.6;
   o->omega_scale = 1.0;
   o->omega_ki = 0.0;
   o->omega_kd = 0.0;
