@@ -206,6 +206,25 @@ int teccl_check_te(teccl_ctx* ctx, const teccl_te_desc* desc, const double* x_ho
 int teccl_check_te_dev(teccl_ctx* ctx, const teccl_te_desc* desc, const double* x_dev,
                        int64_t quantum, int64_t slack_units, teccl_check_report* out);
 
+/* ---------------------------------------------------------------------------
+ * Rate -> schedule decomposition (host CPU, one thread per source). Replaces
+ * lp_rates_to_schedule (pkg/src/collsched/lp.py:156-301) on an LP solution x
+ * in the builder's variable order. in_ptr/in_edges: in-edges of every node in
+ * str(sender) order; pair_chunk_ptr/pair_chunks: demanded chunk ids of every
+ * pair in (str(source), chunk, str(dst)) order; pair_order: pairs in the order
+ * the reference visits them; source_rank/node_rank: positions in str() order.
+ * tol: entries at or below it count as empty while tracing; need_tol: unserved
+ * remainder accepted per chunk. On success *out holds the merged, sorted
+ * events; teccl_schedule_fetch copies them out (src_slot = source slot,
+ * edge = edge index) and frees the handle. */
+int teccl_schedule_te(const teccl_te_desc* desc, const double* x, double tol, double need_tol,
+                      const int32_t* in_ptr, const int32_t* in_edges,
+                      const int32_t* pair_chunk_ptr, const int32_t* pair_chunks,
+                      const int32_t* pair_order, const int32_t* source_rank,
+                      const int32_t* node_rank, int32_t threads, void** out, int64_t* n_events);
+int teccl_schedule_fetch(void* handle, int32_t* src_slot, int32_t* chunk, int32_t* edge,
+                         int32_t* epoch, double* frac);
+
 #ifdef __cplusplus
 }
 #endif

@@ -23,6 +23,7 @@ EXPORTED = (
     "teccl_lp_export", "teccl_lp_export_csc", "teccl_lp_destroy",
     "teccl_pdlp_default_opts", "teccl_pdlp_solve", "teccl_pdlp_solve_dev",
     "teccl_spmv_bench", "teccl_pdlp_step_bench", "teccl_check_te", "teccl_check_te_dev",
+    "teccl_schedule_te", "teccl_schedule_fetch",
 )
 
 STATUS = {0: "optimal", 1: "iteration-limit", 2: "time-limit", 3: "primal-infeasible",
@@ -125,6 +126,12 @@ def load(path: str | None = None):
                                          _p(CheckReport)]),
             "teccl_check_te_dev": (C.c_int, [vp, _p(TeDesc), vp, C.c_int64, C.c_int64,
                                              _p(CheckReport)]),
+            "teccl_schedule_te": (C.c_int, [_p(TeDesc), _p(C.c_double), C.c_double, C.c_double,
+                                            _p(C.c_int32), _p(C.c_int32), _p(C.c_int32),
+                                            _p(C.c_int32), _p(C.c_int32), _p(C.c_int32),
+                                            _p(C.c_int32), C.c_int32, _p(vp), _p(C.c_int64)]),
+            "teccl_schedule_fetch": (C.c_int, [vp, _p(C.c_int32), _p(C.c_int32), _p(C.c_int32),
+                                               _p(C.c_int32), _p(C.c_double)]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)

@@ -71,7 +71,7 @@ def lp_rates_to_schedule(sol, t=None, d=None, cfg=None) -> Schedule:
     if max_deficit(plan, x) > EXACT:  # first-order solution: make every read traceable
         x = repair_flows(plan, x)
         tol = DUST
-    events = decompose(plan, x, tol)
+    events = decompose_native(plan, x, tol)
     return Schedule(tau=plan.cfg.tau, events=tuple(events),
                     completion_epoch=lp_completion_epoch(sol), chunk_size=plan.demand.chunk_size)
 
@@ -179,9 +179,65 @@ def repair_flows(plan: LpPlan, x: np.ndarray) -> np.ndarray:
     return y
 
 
+def _str_ranks(items) -> np.ndarray:
+    """Position of every item in str() order (equal strings share a rank)."""
+    keys = [str(v) for v in items]
+    order = sorted(set(keys))
+    pos = {k: i for i, k in enumerate(order)}
+    return np.array([pos[k] for k in keys], dtype=np.int32)
+
+
+def decompose_native(plan: LpPlan, x: np.ndarray, tol: float = TOL, need_tol: float = TOL,
+                     threads: int = 0) -> list:
+    """The decomposition in libteccl_b200 (csrc/schedule.cu, one CPU thread per
+    source); same events as decompose() below."""
+    import ctypes as C
+    from . import _native as nat
+    lib = nat.load()
+    nodes, E = plan.nodes, plan.E
+    order_in = sorted(range(E), key=lambda e: (int(plan.edst[e]), str(nodes[int(plan.esrc[e])])))
+    in_edges = np.array(order_in, dtype=np.int32)
+    in_ptr = np.zeros(len(nodes) + 1, dtype=np.int32)
+    np.add.at(in_ptr, plan.edst.astype(np.int64) + 1, 1)
+    in_ptr = np.cumsum(in_ptr).astype(np.int32)
+    by_pair: dict = {}
+    for s, c, dst in sorted(plan.demand.entries, key=lambda e: (str(e[0]), e[1], str(e[2]))):
+        by_pair.setdefault((s, dst), []).append(c)
+    pair_index = {pair: p for p, (pair, _) in enumerate(plan.pairs)}
+    chunks = [by_pair.get(pair, []) for pair, _ in plan.pairs]
+    pcp = np.zeros(plan.P + 1, dtype=np.int32)
+    pcp[1:] = np.cumsum([len(c) for c in chunks])
+    pch = np.array([c for cs in chunks for c in cs], dtype=np.int32)
+    porder = np.array([pair_index[pair] for pair, _ in sorted(by_pair.items(), key=str)],
+                      dtype=np.int32)
+    srank = _str_ranks(plan.sources)
+    nrank = _str_ranks(nodes)
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    h = C.c_void_p()
+    cnt = C.c_int64()
+    nat.check(lib.teccl_schedule_te(
+        C.byref(plan.desc()), nat.ptr(x, C.c_double), float(tol), float(need_tol),
+        nat.ptr(in_ptr, C.c_int32), nat.ptr(in_edges, C.c_int32), nat.ptr(pcp, C.c_int32),
+        nat.ptr(pch if pch.size else np.zeros(1, np.int32), C.c_int32),
+        nat.ptr(porder if porder.size else np.zeros(1, np.int32), C.c_int32),
+        nat.ptr(srank if srank.size else np.zeros(1, np.int32), C.c_int32),
+        nat.ptr(nrank, C.c_int32), int(threads), C.byref(h), C.byref(cnt)))
+    n = cnt.value
+    ss, cc, ee, kk = (np.empty(max(n, 1), np.int32) for _ in range(4))
+    ff = np.empty(max(n, 1), np.float64)
+    nat.check(lib.teccl_schedule_fetch(h, nat.ptr(ss, C.c_int32), nat.ptr(cc, C.c_int32),
+                                       nat.ptr(ee, C.c_int32), nat.ptr(kk, C.c_int32),
+                                       nat.ptr(ff, C.c_double)))
+    src = plan.sources
+    return [ScheduleEvent(src[int(ss[i])], int(cc[i]), nodes[int(plan.esrc[ee[i]])],
+                          nodes[int(plan.edst[ee[i]])], int(kk[i]), float(ff[i])) for i in range(n)]
+
+
 def decompose(plan: LpPlan, x: np.ndarray, tol: float = TOL, need_tol: float = TOL) -> list:
-    """tol: entries at or below it count as empty while tracing (the
-    reference's 1e-6); need_tol: unserved remainder accepted per chunk."""
+    """Readable restatement of the reference's decomposition (lp.py:156-301),
+    kept as the specification the native version is tested against. tol:
+    entries at or below it count as empty while tracing (the reference's 1e-6);
+    need_tol: unserved remainder accepted per chunk."""
     K, E = plan.K, plan.E
     nodes = plan.nodes
     esrc, edst, delta = plan.esrc, plan.edst, plan.delta

@@ -91,3 +91,28 @@ def test_repair_makes_perturbed_solution_decomposable():
     rep = simulate([(e.source, e.chunk, e.src, e.dst, e.epoch, e.fraction) for e in events],
                    tau, d.chunk_size, t, d.entries)
     assert rep["violations"] == []
+
+
+@pytest.mark.parametrize("name", SCHEDULED)
+def test_native_decomposition_matches_reference_exactly(name):
+    import os
+    from paper_2305_13479_b200 import _native
+    if not os.path.exists(_native.LIB_PATH):
+        pytest.skip("libteccl_b200.so not built")
+    from paper_2305_13479_b200.schedule import decompose_native
+    meta, gold = load_golden(name)
+    events = decompose_native(_plan(name), gold["x"])
+    got = [[e.source, e.chunk, e.src, e.dst, e.epoch, e.fraction] for e in events]
+    assert got == meta["schedule"]
+
+
+def test_native_and_python_agree_after_repair():
+    import numpy as np
+    from paper_2305_13479_b200.schedule import DUST, decompose_native, repair_flows
+    meta, gold = load_golden("dgx2x1_a2a_K20")
+    plan = _plan("dgx2x1_a2a_K20")
+    rng = np.random.default_rng(1)
+    y = repair_flows(plan, gold["x"] * (1.0 + 1e-7 * rng.standard_normal(gold["x"].shape)))
+    a = decompose(plan, y, DUST)
+    b = decompose_native(plan, y, DUST)
+    assert a == b

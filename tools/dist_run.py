@@ -24,6 +24,7 @@ chunks = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 K = int(sys.argv[3]) if len(sys.argv) > 3 else 530
 eps = float(sys.argv[4]) if len(sys.argv) > 4 else 1e-4
 compare = int(sys.argv[5]) if len(sys.argv) > 5 else 1
+max_iters = int(sys.argv[6]) if len(sys.argv) > 6 else 5_000_000
 local = int(os.environ.get("LOCAL_RANK", "0"))
 torch.cuda.set_device(local)
 dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
@@ -33,7 +34,8 @@ t = ndv2(chassis)
 d = generate_demand("allgather", t, chunks, 25000)
 cfg = EpochConfig(epoch_duration(t, d.chunk_size, "fastest", 1), K, "fastest", 1, d.chunk_size)
 t0 = time.perf_counter()
-out = solve_partitioned(t, d, cfg, eps_rel=eps, device=local, gather=bool(compare))
+out = solve_partitioned(t, d, cfg, eps_rel=eps, device=local, gather=bool(compare),
+                        max_iters=max_iters)
 wall = time.perf_counter() - t0
 secs = torch.tensor([out["device_seconds"]], dtype=torch.float64, device=f"cuda:{local}")
 dist.all_reduce(secs, op=dist.ReduceOp.MAX)
