@@ -286,8 +286,8 @@ extern "C" int teccl_lp_destroy(teccl_lp* lp) {
   if (lp->dist && lp->dist_free) lp->dist_free(lp->dist);
   void* ptrs[] = {lp->row_ptr, lp->col, lp->val, lp->col_ptr, lp->row, lp->cval,
                   lp->row_lo, lp->row_hi, lp->var_lb, lp->var_ub, lp->obj,
-                  lp->srow_off, lp->srow_w, lp->srow_idx, lp->srow_val,
-                  lp->scol_off, lp->scol_w, lp->scol_idx, lp->scol_val,
+                  lp->srow_off, lp->srow_w, lp->sell_idx, lp->srow_val,
+                  lp->scol_off, lp->scol_w, lp->scol_val,
                   lp->col_code, lp->row_code, lp->col_dict, lp->row_dict};
   for (void* p : ptrs)
     if (p) {

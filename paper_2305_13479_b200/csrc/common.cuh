@@ -81,6 +81,8 @@ struct teccl_lp {
   uint32_t* scol_idx = nullptr;
   double* scol_val = nullptr;
   int64_t srow_entries = 0, scol_entries = 0;
+  uint32_t* sell_idx = nullptr;    // one allocation: [srow_idx | scol_idx]
+  size_t sell_idx_bytes = 0;
   // bound classes: uint16 code per column/row into (lb,ub,c) / (lo,hi)
   // dictionaries; nullptr when the LP has too many distinct classes
   uint16_t* col_code = nullptr;

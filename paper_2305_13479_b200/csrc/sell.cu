@@ -50,14 +50,15 @@ __global__ void sell_fill_kernel(int64_t count, int64_t nslices, const int64_t* 
   }
 }
 
-static int build_one(int64_t count, const int64_t* ptr, const uint32_t* idx, const double* val,
-                     uint32_t sentinel, cudaStream_t st, int64_t** off, int32_t** width,
-                     uint32_t** sidx, double** sval, int64_t* entries) {
+// Slice widths and offsets of one orientation; *entries = stored entries.
+static int sell_layout(int64_t count, const int64_t* ptr, cudaStream_t st, int64_t** off,
+                       int32_t** width, int64_t* entries) {
   const int64_t ns = (count + 31) / 32;
   int64_t* slice_len = nullptr;
   TECCL_CUDA(cudaMallocAsync((void**)off, sizeof(int64_t) * (ns + 1), st));
   TECCL_CUDA(cudaMallocAsync((void**)width, sizeof(int32_t) * (ns + 1), st));
   TECCL_CUDA(cudaMallocAsync((void**)&slice_len, sizeof(int64_t) * (ns + 1), st));
+  int64_t total = 0;
   if (ns > 0) {
     sell_width_kernel<<<(int)((ns * 32 + 255) / 256), 256, 0, st>>>(count, ns, ptr, *width, slice_len);
     TECCL_CHECK_LAUNCH();
@@ -69,20 +70,24 @@ static int build_one(int64_t count, const int64_t* ptr, const uint32_t* idx, con
     cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, slice_len, *off, ns + 1, st);
     TECCL_CHECK_LAUNCH();
     TECCL_CUDA(cudaFreeAsync(tmp, st));
-  }
-  int64_t total = 0;
-  if (ns > 0)
     TECCL_CUDA(cudaMemcpyAsync(&total, *off + ns, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  TECCL_CUDA(cudaStreamSynchronize(st));
-  TECCL_CUDA(cudaMallocAsync((void**)sidx, sizeof(uint32_t) * (total + 4), st));
-  if (val) TECCL_CUDA(cudaMallocAsync((void**)sval, sizeof(double) * (total + 4), st));
-  if (ns > 0) {
-    sell_fill_kernel<<<(int)((ns * 32 + 255) / 256), 256, 0, st>>>(
-        count, ns, ptr, idx, val, *off, *width, sentinel, *sidx, val ? *sval : nullptr);
-    TECCL_CHECK_LAUNCH();
   }
   TECCL_CUDA(cudaFreeAsync(slice_len, st));
+  TECCL_CUDA(cudaStreamSynchronize(st));
   *entries = total;
+  return TECCL_OK;
+}
+
+static int sell_fill(int64_t count, const int64_t* ptr, const uint32_t* idx, const double* val,
+                     uint32_t sentinel, cudaStream_t st, const int64_t* off, const int32_t* width,
+                     uint32_t* sidx, double** sval, int64_t entries) {
+  const int64_t ns = (count + 31) / 32;
+  if (val) TECCL_CUDA(cudaMallocAsync((void**)sval, sizeof(double) * (entries + 4), st));
+  if (ns > 0) {
+    sell_fill_kernel<<<(int)((ns * 32 + 255) / 256), 256, 0, st>>>(
+        count, ns, ptr, idx, val, off, width, sentinel, sidx, val ? *sval : nullptr);
+    TECCL_CHECK_LAUNCH();
+  }
   return TECCL_OK;
 }
 
@@ -91,11 +96,22 @@ static int build_one(int64_t count, const int64_t* ptr, const uint32_t* idx, con
 int teccl_build_sell(teccl_lp* lp, cudaStream_t st) {
   using namespace teccl;
   if (lp->sell_ready) return TECCL_OK;
-  int rc = build_one(lp->m, lp->row_ptr, lp->col, lp->unit ? nullptr : lp->val, (uint32_t)gather_cols(lp),
-                     st, &lp->srow_off, &lp->srow_w, &lp->srow_idx, &lp->srow_val, &lp->srow_entries);
+  int rc = sell_layout(lp->m, lp->row_ptr, st, &lp->srow_off, &lp->srow_w, &lp->srow_entries);
   if (rc) return rc;
-  rc = build_one(lp->n, lp->col_ptr, lp->row, lp->unit ? nullptr : lp->cval, (uint32_t)gather_rows(lp), st,
-                 &lp->scol_off, &lp->scol_w, &lp->scol_idx, &lp->scol_val, &lp->scol_entries);
+  rc = sell_layout(lp->n, lp->col_ptr, st, &lp->scol_off, &lp->scol_w, &lp->scol_entries);
+  if (rc) return rc;
+  // both index streams in one allocation, so one L2 access-policy window
+  // can cover them (pdlp.cu keeps them L2-resident across iterations)
+  const int64_t rpad = (lp->srow_entries + 63) / 64 * 64;
+  TECCL_CUDA(cudaMallocAsync((void**)&lp->sell_idx, sizeof(uint32_t) * (rpad + lp->scol_entries + 64), st));
+  lp->srow_idx = lp->sell_idx;
+  lp->scol_idx = lp->sell_idx + rpad;
+  lp->sell_idx_bytes = sizeof(uint32_t) * (rpad + lp->scol_entries);
+  rc = sell_fill(lp->m, lp->row_ptr, lp->col, lp->unit ? nullptr : lp->val, (uint32_t)gather_cols(lp),
+                 st, lp->srow_off, lp->srow_w, lp->srow_idx, &lp->srow_val, lp->srow_entries);
+  if (rc) return rc;
+  rc = sell_fill(lp->n, lp->col_ptr, lp->row, lp->unit ? nullptr : lp->cval, (uint32_t)gather_rows(lp),
+                 st, lp->scol_off, lp->scol_w, lp->scol_idx, &lp->scol_val, lp->scol_entries);
   if (rc) return rc;
   TECCL_CUDA(cudaStreamSynchronize(st));
   lp->sell_ready = true;
