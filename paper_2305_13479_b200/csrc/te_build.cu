@@ -585,10 +585,6 @@ int prepare_tables(teccl_ctx* ctx, const teccl_te_desc* desc, TeDev& d, std::vec
   d.n_rows = d.R_bcap + (d.has_bcap ? (int64_t)G * (K + 1) : 0);
   d.n_vars = (int64_t)S * d.SB + (int64_t)P * 2 * K;
   if (S == 0) d.CB = 0;
-  if (d.n_vars >= (int64_t)kSignBit || d.n_rows >= (int64_t)kSignBit) {
-    set_error("LP too large for 31-bit indices on one device; row-partition it");
-    return TECCL_EINVAL;
-  }
 
   // Upload the small tables.
   std::vector<uint8_t> is_sw(desc->node_is_switch, desc->node_is_switch + Nn);
@@ -708,6 +704,11 @@ extern "C" int teccl_lp_build_te(teccl_ctx* ctx, const teccl_te_desc* desc, tecc
   cudaStream_t st = ctx->stream;
   int prc = prepare_tables(ctx, desc, d, owned);
   if (prc) { for (void* p : owned) cudaFreeAsync(p, st); return prc; }
+  if (d.n_vars >= (int64_t)kSignBit || d.n_rows >= (int64_t)kSignBit) {
+    for (void* p : owned) cudaFreeAsync(p, st);
+    set_error("LP too large for 31-bit indices on one device; row-partition it");
+    return TECCL_EINVAL;
+  }
   teccl_lp* lp = new teccl_lp();
   lp->m = (int32_t)d.n_rows;
   lp->n = (int32_t)d.n_vars;
