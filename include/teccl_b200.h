@@ -144,6 +144,7 @@ typedef struct {
   double omega_scale;         /* multiplies the initial primal weight (1.0) */
   double omega_ki;            /* integral gain of the primal-weight PID (0) */
   double omega_kd;            /* derivative gain of the primal-weight PID (0) */
+  int32_t col_pipeline;       /* 1: software-pipelined column half-step kernel (1) */
 } teccl_pdlp_opts;
 
 typedef struct {

@@ -53,7 +53,7 @@ class PdlpOpts(C.Structure):
         ("warm_start", C.c_int32), ("restart_sufficient", C.c_double),
         ("restart_necessary", C.c_double), ("restart_artificial", C.c_double),
         ("omega_theta", C.c_double), ("omega_scale", C.c_double),
-        ("omega_ki", C.c_double), ("omega_kd", C.c_double),
+        ("omega_ki", C.c_double), ("omega_kd", C.c_double), ("col_pipeline", C.c_int32),
     ]
 
 

@@ -85,6 +85,7 @@ struct Vecs {
   PdlpState* st;
   double* slots;         // [world][kSlots]: every rank's reduced partials
   int world, rank;
+  int col_pipe;          // column half-step: pipelined resident grid (1) or one thread per column (0)
 };
 
 __device__ __forceinline__ double block_sum(double v, double* sh);
@@ -350,6 +351,95 @@ __global__ void __launch_bounds__(kThreads) col_step_kernel(int32_t n, SellView 
       dx = (xt - xj) * (xt - xj) * w;
       dx0 = (xt - x0) * (xt - x0) * w;
     }
+  }
+  if (CHECK) {
+    double a = block_sum(dx, sh);
+    if (threadIdx.x == 0) V.part[Q_DX * V.pstride + blockIdx.x] = a;
+    a = block_sum(dx0, sh);
+    if (threadIdx.x == 0) V.part[Q_DX0 * V.pstride + blockIdx.x] = a;
+  }
+}
+
+// Software-pipelined variant of col_step: a resident grid walks the columns
+// with a grid stride; while a thread gathers and updates column j, the slice
+// header and index loads of its next column j + stride are already in
+// flight, so each column costs about one memory latency instead of three.
+template <bool UNIT, bool DICT, bool CHECK>
+__global__ void __launch_bounds__(kThreads) col_pipe_kernel(int32_t n, SellView S, Vecs V,
+                                                            int j_in_chunk) {
+  __shared__ double sh[32];
+  const PdlpState* st = V.st;
+  if (st->done) return;
+  const double tau = st->tau, refl = st->refl;
+  const double kk = (double)(st->k_inner + j_in_chunk);
+  const double lam = (kk + 1.0) / (kk + 2.0);
+  const int64_t stride = (int64_t)gridDim.x * kThreads;
+  int64_t j = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  // stage 1 of the first column: slice header and up to 4 indices
+  int w = 0;
+  int64_t base = 0;
+  uint32_t t[4] = {0u, 0u, 0u, 0u};
+  if (j < n) {
+    w = __ldg(S.width + (j >> 5));
+    base = __ldg(S.off + (j >> 5)) + (j & 31);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) t[u] = (u < w) ? __ldg(S.idx + base + (int64_t)u * kSlice) : 0u;
+  }
+  double dx = 0.0, dx0 = 0.0;
+  while (j < n) {
+    const int64_t jn = j + stride;
+    // next column's slice header: independent of this column's work
+    int wn = 0;
+    int64_t basen = 0;
+    if (jn < n) {
+      wn = __ldg(S.width + (jn >> 5));
+      basen = __ldg(S.off + (jn >> 5)) + (jn & 31);
+    }
+    // this column: epilogue operands and gathers
+    double lb, ub, cj;
+    col_data<DICT>(V.col, j, lb, ub, cj);
+    const double xj = V.x[j];
+    const double x0 = (double)V.x0[j];
+    const double Dj = (double)V.D[j];
+    double s = 0.0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (u < w) {
+        if (UNIT) {
+          const double xv = __ldg(V.y + (t[u] & kIdxMask));
+          s += (t[u] & kSignBit) ? -xv : xv;
+        } else {
+          s += __ldg(S.val + base + (int64_t)u * kSlice) * __ldg(V.y + t[u]);
+        }
+      }
+    }
+    for (int q = 4; q < w; ++q) {  // columns wider than 4 (rare)
+      const uint32_t tq = __ldg(S.idx + base + (int64_t)q * kSlice);
+      if (UNIT) {
+        const double xv = __ldg(V.y + (tq & kIdxMask));
+        s += (tq & kSignBit) ? -xv : xv;
+      } else {
+        s += __ldg(S.val + base + (int64_t)q * kSlice) * __ldg(V.y + tq);
+      }
+    }
+    // next column's indices (its header has had a whole gather to arrive)
+    uint32_t tn[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+    for (int u = 0; u < 4; ++u) tn[u] = (u < wn) ? __ldg(S.idx + basen + (int64_t)u * kSlice) : 0u;
+    const double xt = clampd(xj - tau * Dj * (cj - s), lb, ub);
+    V.xbar[j] = 2.0 * xt - xj;
+    V.x[j] = lam * ((1.0 + refl) * xt - refl * xj) + (1.0 - lam) * x0;
+    if (CHECK) {
+      V.xt[j] = xt;
+      const double wgt = 1.0 / Dj;
+      dx += (xt - xj) * (xt - xj) * wgt;
+      dx0 += (xt - x0) * (xt - x0) * wgt;
+    }
+    j = jn;
+    w = wn;
+    base = basen;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) t[u] = tn[u];
   }
   if (CHECK) {
     double a = block_sum(dx, sh);
@@ -793,7 +883,7 @@ struct Workspace {
   PdlpState* dst = nullptr;
   int64_t pstride = 0;
   cudaGraphExec_t gexec = nullptr;
-  int graph_chunk = 0;
+  int graph_chunk = 0;  // key of the captured graph: chunk length and kernel variant
   PdlpState* ring = nullptr;
   int ring_len = 0;
   std::vector<cudaEvent_t> evs;
@@ -838,9 +928,25 @@ SellView col_view(const teccl_lp* lp) {
   return SellView{lp->scol_off, lp->scol_w, lp->scol_idx, lp->scol_val, lp->n};
 }
 
+// blocks of the pipelined column kernel: every SM full, one pass
+int pipe_blocks() {
+  static int blocks = 0;
+  if (!blocks) {
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, col_pipe_kernel<true, true, false>, kThreads, 0);
+    blocks = kSMs * (occ > 0 ? occ : 4);
+  }
+  return blocks;
+}
+
 template <bool UNIT, bool DICT, bool CHECK>
 void launch_col(cudaStream_t st, const teccl_lp* lp, const Vecs& V, int j) {
-  col_step_kernel<UNIT, DICT, CHECK><<<V.nb_col, kThreads, 0, st>>>(lp->n, col_view(lp), V, j);
+  if (V.col_pipe) {
+    const int blocks = std::min<int>(pipe_blocks(), V.nb_col);
+    col_pipe_kernel<UNIT, DICT, CHECK><<<blocks, kThreads, 0, st>>>(lp->n, col_view(lp), V, j);
+  } else {
+    col_step_kernel<UNIT, DICT, CHECK><<<V.nb_col, kThreads, 0, st>>>(lp->n, col_view(lp), V, j);
+  }
 }
 template <bool UNIT, bool DICT, bool CHECK>
 void launch_row(cudaStream_t st, const teccl_lp* lp, const Vecs& V, int j) {
@@ -1093,6 +1199,9 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
   TECCL_CHECK_LAUNCH();
 
   mark("power-iter");
+  // the setup reductions used the partial slots; the iteration kernels write
+  // only as many slots as they have blocks, so start them from zero
+  TECCL_CUDA(cudaMemsetAsync(part, 0, sizeof(double) * kNQ * pstride, st));
   // --- state: omega in original space = scaled weight * gamma / beta
   PdlpState hs{};
   hs.eta = 0.998 / sigma_max;
@@ -1127,6 +1236,7 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
   V.slots = slots;
   V.world = world;
   V.rank = rank;
+  V.col_pipe = o->col_pipeline;
   // Vc: column kernels (own x side, gather y windows); Vr: row kernels
   // (own y side, gather x windows); Vi: owned parts only
   Vecs Vc = V, Vr = V, Vi = V;
@@ -1173,7 +1283,8 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
   }
 
   // --- chunk graph (captured once per LP and chunk length)
-  if (o->use_graphs && W.gexec && W.graph_chunk != chunk) {
+  const int graph_key = chunk * 2 + (o->col_pipeline ? 1 : 0);
+  if (o->use_graphs && W.gexec && W.graph_chunk != graph_key) {
     cudaGraphExecDestroy(W.gexec);
     W.gexec = nullptr;
   }
@@ -1190,7 +1301,7 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
     TECCL_CUDA(cudaGraphInstantiate(&W.gexec, g, 0));
     TECCL_CUDA(cudaGraphDestroy(g));
     TECCL_CUDA(cudaStreamDestroy(cap));
-    W.graph_chunk = chunk;
+    W.graph_chunk = graph_key;
   }
   cudaGraphExec_t gexec = o->use_graphs ? W.gexec : nullptr;
   per_chunk = 2LL * chunk + 6 + (X.active() ? 4LL * chunk + 1 : 0);
@@ -1313,6 +1424,7 @@ extern "C" void teccl_pdlp_default_opts(teccl_pdlp_opts* o) {
   o->omega_scale = 1.0;
   o->omega_ki = 0.0;
   o->omega_kd = 0.0;
+  o->col_pipeline = 1;
 }
 
 extern "C" int teccl_pdlp_solve_dev(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* opts,
