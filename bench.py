@@ -226,7 +226,8 @@ def run_b200(args, rank, world, local_rank):
         parity["reference_highs_seconds"] = gold["highs_ipm_seconds"]
     # --- roofline of the dominant fused kernel (live CUDA-event timing)
     sb = lp.step_bench(200)
-    kern = "row_step_kernel" if sb["ms_row"] >= sb["ms_col"] else "col_step_kernel"
+    col_name = "col_pipe_kernel"  # default column half-step (teccl_pdlp_opts.col_pipeline = 1)
+    kern = "row_step_kernel" if sb["ms_row"] >= sb["ms_col"] else col_name
     ms = max(sb["ms_row"], sb["ms_col"])
     by = sb["bytes_row"] if kern == "row_step_kernel" else sb["bytes_col"]
     peak, peak_kind = peaks()
