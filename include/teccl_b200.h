@@ -145,6 +145,12 @@ typedef struct {
   double omega_ki;            /* integral gain of the primal-weight PID (0) */
   double omega_kd;            /* derivative gain of the primal-weight PID (0) */
   int32_t col_pipeline;       /* 1: software-pipelined column half-step kernel (1) */
+  int32_t matrix_free;        /* LPs from teccl_lp_build_te apply A / A^T from the
+                                 topology tables instead of the stored matrix:
+                                 0 off, 1 auto (segment kernels when K >= 16, else
+                                 per-entry), 2 per-entry, 3 segment kernels (0) */
+  int32_t pdl;                /* 1: programmatic dependent launch between the iteration
+                                 kernels (prologue of one overlaps the tail of the last) (1) */
 } teccl_pdlp_opts;
 
 typedef struct {
@@ -177,10 +183,21 @@ int teccl_pdlp_solve_dev(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* op
 int teccl_spmv_bench(teccl_ctx* ctx, teccl_lp* lp, int32_t reps, double* ms_per_pair,
                      double* bytes_per_pair);
 
+/* out = A.in (transpose = 0, length m) or A^T.in (transpose = 1, length n)
+ * through the stored CSR/CSC (matrix_free = 0) or, for LPs from
+ * teccl_lp_build_te, the per-entry matrix-free operator (1) or the segment
+ * walkers the PDLP kernels use (2), with the row bounds /
+ * column bounds and costs that path uses (lo/hi/cost may be NULL; cost only
+ * for transpose = 1). Host buffers. The parity tests pin the two paths to
+ * each other bit for bit. */
+int teccl_lp_apply(teccl_ctx* ctx, teccl_lp* lp, int32_t transpose, int32_t matrix_free,
+                   const double* in, double* out, double* lo, double* hi, double* cost);
+
 /* Time the two fused PDLP iteration kernels alone (after the real scaling
  * setup), `reps` launches each, CUDA events on the context stream.
- * out6 = {ms per col_step launch, ms per row_step launch, algorithmic bytes
- * per col_step launch, per row_step launch, col group size, row group size}. */
+ * out6 = {ms per column-kernel launch, ms per row-kernel launch, algorithmic
+ * bytes per column launch, per row launch, operator (2 matrix-free, 1 stored
+ * matrix + bound dictionaries, 0 stored + bound arrays), SELL slice}. */
 int teccl_pdlp_step_bench(teccl_ctx* ctx, teccl_lp* lp, int32_t reps, double* out6);
 
 /* ---------------------------------------------------------------------------

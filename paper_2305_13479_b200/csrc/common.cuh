@@ -105,6 +105,10 @@ struct teccl_lp {
   int64_t nnz_csc = -1;            // CSC entries when they differ from nnz
   void* dist = nullptr;            // peer-memory exchange state (pdlp.cu)
   void (*dist_free)(void*) = nullptr;
+  // structure tables of a single-device TE LP (teccl::TeHold, te_gen.cuh):
+  // lets the PDLP kernels apply A / A^T without reading the stored matrix
+  void* te = nullptr;
+  void (*te_free)(void*) = nullptr;
 };
 
 // lengths of the vectors the SpMVs gather from, and where the owned part

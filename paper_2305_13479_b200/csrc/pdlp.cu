@@ -39,6 +39,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "te_gen.cuh"
 
 namespace teccl {
 
@@ -86,6 +87,8 @@ struct Vecs {
   double* slots;         // [world][kSlots]: every rank's reduced partials
   int world, rank;
   int col_pipe;          // column half-step: pipelined resident grid (1) or one thread per column (0)
+  int pdl;               // iteration kernels launched with programmatic dependent launch
+  int seg;               // matrix-free: segment-walking kernels (1) or one thread per entry (0)
 };
 
 __device__ __forceinline__ double block_sum(double v, double* sh);
@@ -288,6 +291,15 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
   return t;  // valid in thread 0
 }
 
+// Programmatic dependent launch (PDL): the iteration kernels are launched
+// with programmatic stream serialization, so a kernel's blocks may start
+// while its predecessor drains. Everything before pdl_wait() reads only
+// data final at least two launches back (dense iterates, constant tables);
+// the predecessor's outputs and the solver state are read after it.
+// Without the launch attribute both instructions are no-ops.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ double clampd(double v, double lo, double hi) {
   return fmin(fmax(v, lo), hi);
 }
@@ -325,11 +337,6 @@ template <bool UNIT, bool DICT, bool CHECK>
 __global__ void __launch_bounds__(kThreads) col_step_kernel(int32_t n, SellView S, Vecs V,
                                                             int j_in_chunk) {
   __shared__ double sh[32];
-  const PdlpState* st = V.st;
-  if (st->done) return;
-  const double tau = st->tau, refl = st->refl;
-  const double kk = (double)(st->k_inner + j_in_chunk);
-  const double lam = (kk + 1.0) / (kk + 2.0);
   const int64_t j = (int64_t)blockIdx.x * kTile + threadIdx.x;
   // operands of the epilogue do not depend on the SpMV: load them first
   double xj = 0.0, x0 = 0.0, Dj = 0.0, lb = 0.0, ub = 0.0, cj = 0.0;
@@ -339,7 +346,15 @@ __global__ void __launch_bounds__(kThreads) col_step_kernel(int32_t n, SellView 
     Dj = (double)V.D[j];
     col_data<DICT>(V.col, j, lb, ub, cj);
   }
+  pdl_wait();
+  pdl_trigger();
+  const PdlpState* st = V.st;
+  const int done = st->done;  // checked before the first store: the gathers overlap it
+  const double tau = st->tau, refl = st->refl;
+  const double kk = (double)(st->k_inner + j_in_chunk);
+  const double lam = (kk + 1.0) / (kk + 2.0);
   const double s = (j < n) ? sell_dot<UNIT>(S, j, V.y) : 0.0;
+  if (done) return;
   double dx = 0.0, dx0 = 0.0;
   if (j < n) {
     const double xt = clampd(xj - tau * Dj * (cj - s), lb, ub);
@@ -368,11 +383,6 @@ template <bool UNIT, bool DICT, bool CHECK>
 __global__ void __launch_bounds__(kThreads) col_pipe_kernel(int32_t n, SellView S, Vecs V,
                                                             int j_in_chunk) {
   __shared__ double sh[32];
-  const PdlpState* st = V.st;
-  if (st->done) return;
-  const double tau = st->tau, refl = st->refl;
-  const double kk = (double)(st->k_inner + j_in_chunk);
-  const double lam = (kk + 1.0) / (kk + 2.0);
   const int64_t stride = (int64_t)gridDim.x * kThreads;
   int64_t j = (int64_t)blockIdx.x * kThreads + threadIdx.x;
   // stage 1 of the first column: slice header and up to 4 indices
@@ -385,6 +395,14 @@ __global__ void __launch_bounds__(kThreads) col_pipe_kernel(int32_t n, SellView 
 #pragma unroll
     for (int u = 0; u < 4; ++u) t[u] = (u < w) ? __ldg(S.idx + base + (int64_t)u * kSlice) : 0u;
   }
+  pdl_wait();
+  pdl_trigger();
+  const PdlpState* st = V.st;
+  const int done = st->done;
+  const double tau = st->tau, refl = st->refl;
+  const double kk = (double)(st->k_inner + j_in_chunk);
+  const double lam = (kk + 1.0) / (kk + 2.0);
+  if (done) return;
   double dx = 0.0, dx0 = 0.0;
   while (j < n) {
     const int64_t jn = j + stride;
@@ -454,11 +472,6 @@ template <bool UNIT, bool DICT, bool CHECK>
 __global__ void __launch_bounds__(kThreads) row_step_kernel(int32_t m, SellView S, Vecs V,
                                                             int j_in_chunk) {
   __shared__ double sh[32];
-  const PdlpState* st = V.st;
-  if (st->done) return;
-  const double sigma = st->sigma, refl = st->refl;
-  const double kk = (double)(st->k_inner + j_in_chunk);
-  const double lam = (kk + 1.0) / (kk + 2.0);
   const int64_t i = (int64_t)blockIdx.x * kTile + threadIdx.x;
   double yi = 0.0, y0 = 0.0, Ei = 0.0, lo = 0.0, hi = 0.0;
   if (i < m) {
@@ -467,7 +480,15 @@ __global__ void __launch_bounds__(kThreads) row_step_kernel(int32_t m, SellView 
     Ei = (double)V.E[i];
     row_data<DICT>(V.row, i, lo, hi);
   }
+  pdl_wait();
+  pdl_trigger();
+  const PdlpState* st = V.st;
+  const int done = st->done;  // checked before the first store: the gathers overlap it
+  const double sigma = st->sigma, refl = st->refl;
+  const double kk = (double)(st->k_inner + j_in_chunk);
+  const double lam = (kk + 1.0) / (kk + 2.0);
   const double s = (i < m) ? sell_dot<UNIT, 8>(S, i, V.xbar) : 0.0;
+  if (done) return;
   double dy = 0.0, dy0 = 0.0;
   if (i < m) {
     const double se = sigma * Ei;
@@ -488,17 +509,219 @@ __global__ void __launch_bounds__(kThreads) row_step_kernel(int32_t m, SellView 
   }
 }
 
+// ---------------------------------------------------------------------------
+// Matrix-free half-steps for LPs built by teccl_lp_build_te: the same
+// updates as col_step / row_step, with A^T y and A x evaluated from the
+// topology tables (te_gen.cuh) and the bounds/costs computed in place. No
+// index or bound-class stream: HBM traffic is the dense vectors plus the
+// gathered operand, whose accesses are coalesced along the epoch axis.
+template <bool CHECK>
+__global__ void __launch_bounds__(kThreads) col_te_kernel(TeOp op, Vecs V, int j_in_chunk) {
+  __shared__ double sh[32];
+  const uint32_t j = blockIdx.x * kTile + threadIdx.x;
+  double xj = 0.0, x0 = 0.0, Dj = 1.0, lb = 0.0, ub = 0.0, cj = 0.0, s = 0.0;
+  if (j < op.n) {
+    xj = V.x[j];
+    x0 = (double)V.x0[j];
+    Dj = (double)V.D[j];
+  }
+  pdl_wait();
+  pdl_trigger();
+  const PdlpState* st = V.st;
+  const int done = st->done;  // checked before the first store: the gathers overlap it
+  const double tau = st->tau, refl = st->refl;
+  const double kk = (double)(st->k_inner + j_in_chunk);
+  if (j < op.n) s = te_col(op, j, V.y, lb, ub, cj);
+  if (done) return;
+  const double lam = (kk + 1.0) / (kk + 2.0);
+  double dx = 0.0, dx0 = 0.0;
+  if (j < op.n) {
+    const double xt = clampd(xj - tau * Dj * (cj - s), lb, ub);
+    V.xbar[j] = 2.0 * xt - xj;
+    V.x[j] = lam * ((1.0 + refl) * xt - refl * xj) + (1.0 - lam) * x0;
+    if (CHECK) {
+      V.xt[j] = xt;
+      const double w = 1.0 / Dj;
+      dx = (xt - xj) * (xt - xj) * w;
+      dx0 = (xt - x0) * (xt - x0) * w;
+    }
+  }
+  if (CHECK) {
+    double a = block_sum(dx, sh);
+    if (threadIdx.x == 0) V.part[Q_DX * V.pstride + blockIdx.x] = a;
+    a = block_sum(dx0, sh);
+    if (threadIdx.x == 0) V.part[Q_DX0 * V.pstride + blockIdx.x] = a;
+  }
+}
+
+template <bool CHECK>
+__global__ void __launch_bounds__(kThreads) row_te_kernel(TeOp op, Vecs V, int j_in_chunk) {
+  __shared__ double sh[32];
+  const uint32_t i = blockIdx.x * kTile + threadIdx.x;
+  double yi = 0.0, y0 = 0.0, Ei = 1.0, lo = 0.0, hi = 0.0, s = 0.0;
+  if (i < op.m) {
+    yi = V.y[i];
+    y0 = (double)V.y0[i];
+    Ei = (double)V.E[i];
+  }
+  pdl_wait();
+  pdl_trigger();
+  const PdlpState* st = V.st;
+  const int done = st->done;  // checked before the first store: the gathers overlap it
+  const double sigma = st->sigma, refl = st->refl;
+  const double kk = (double)(st->k_inner + j_in_chunk);
+  if (i < op.m) s = te_row(op, i, V.xbar, lo, hi);
+  if (done) return;
+  const double lam = (kk + 1.0) / (kk + 2.0);
+  double dy = 0.0, dy0 = 0.0;
+  if (i < op.m) {
+    const double se = sigma * Ei;
+    const double yt = yi - se * (s - clampd(s - yi / se, lo, hi));
+    V.y[i] = lam * ((1.0 + refl) * yt - refl * yi) + (1.0 - lam) * y0;
+    if (CHECK) {
+      V.yt[i] = yt;
+      const double w = 1.0 / Ei;
+      dy = (yt - yi) * (yt - yi) * w;
+      dy0 = (yt - y0) * (yt - y0) * w;
+    }
+  }
+  if (CHECK) {
+    double a = block_sum(dy, sh);
+    if (threadIdx.x == 0) V.part[Q_DY * V.pstride + blockIdx.x] = a;
+    a = block_sum(dy0, sh);
+    if (threadIdx.x == 0) V.part[Q_DY0 * V.pstride + blockIdx.x] = a;
+  }
+}
+
+// Segment-walking half-steps (te_gen.cuh seg_cols / seg_rows): one warp per
+// task of up to 64 consecutive entries of one column / row family, so the
+// table lookups are per task and each entry costs only its gathers and the
+// PDHG update. Same updates as col_te / row_te.
+template <bool CHECK>
+__global__ void __launch_bounds__(kThreads) col_seg_kernel(TeOp op, Vecs V, int j_in_chunk) {
+  __shared__ double sh[32];
+  const int wi = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  const int4 tk = (wi < op.n_ctask) ? __ldg(op.ctask + wi) : make_int4(0, 0, 0, 0);
+  const int cnt = seg_count(tk);
+  const uint32_t first = (uint32_t)tk.z;
+  double xj[kSegPerLane], x0[kSegPerLane], Dj[kSegPerLane];
+#pragma unroll
+  for (int h = 0; h < kSegPerLane; ++h) {
+    const int i = lane + 32 * h;
+    xj[h] = 0.0; x0[h] = 0.0; Dj[h] = 1.0;
+    if (i < cnt) {
+      xj[h] = V.x[first + i];
+      x0[h] = (double)V.x0[first + i];
+      Dj[h] = (double)V.D[first + i];
+    }
+  }
+  pdl_wait();
+  pdl_trigger();
+  const PdlpState* st = V.st;
+  const int done = st->done;
+  const double tau = st->tau, refl = st->refl;
+  const double kk = (double)(st->k_inner + j_in_chunk);
+  double s[kSegPerLane], lb[kSegPerLane], ub[kSegPerLane], cj[kSegPerLane];
+  seg_cols(op, tk, lane, V.y, s, lb, ub, cj);
+  if (done) return;
+  const double lam = (kk + 1.0) / (kk + 2.0);
+  double dx = 0.0, dx0 = 0.0;
+#pragma unroll
+  for (int h = 0; h < kSegPerLane; ++h) {
+    const int i = lane + 32 * h;
+    if (i < cnt) {
+      const uint32_t j = first + i;
+      const double xt = clampd(xj[h] - tau * Dj[h] * (cj[h] - s[h]), lb[h], ub[h]);
+      V.xbar[j] = 2.0 * xt - xj[h];
+      V.x[j] = lam * ((1.0 + refl) * xt - refl * xj[h]) + (1.0 - lam) * x0[h];
+      if (CHECK) {
+        V.xt[j] = xt;
+        const double w = 1.0 / Dj[h];
+        dx += (xt - xj[h]) * (xt - xj[h]) * w;
+        dx0 += (xt - x0[h]) * (xt - x0[h]) * w;
+      }
+    }
+  }
+  if (CHECK) {
+    double a = block_sum(dx, sh);
+    if (threadIdx.x == 0) V.part[Q_DX * V.pstride + blockIdx.x] = a;
+    a = block_sum(dx0, sh);
+    if (threadIdx.x == 0) V.part[Q_DX0 * V.pstride + blockIdx.x] = a;
+  }
+}
+
+template <bool CHECK>
+__global__ void __launch_bounds__(kThreads) row_seg_kernel(TeOp op, Vecs V, int j_in_chunk) {
+  __shared__ double sh[32];
+  const int wi = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  const int4 tk = (wi < op.n_rtask) ? __ldg(op.rtask + wi) : make_int4(0, 0, 0, 0);
+  const int cnt = seg_count(tk);
+  const uint32_t first = (uint32_t)tk.z;
+  double yi[kSegPerLane], y0[kSegPerLane], Ei[kSegPerLane];
+#pragma unroll
+  for (int h = 0; h < kSegPerLane; ++h) {
+    const int i = lane + 32 * h;
+    yi[h] = 0.0; y0[h] = 0.0; Ei[h] = 1.0;
+    if (i < cnt) {
+      yi[h] = V.y[first + i];
+      y0[h] = (double)V.y0[first + i];
+      Ei[h] = (double)V.E[first + i];
+    }
+  }
+  pdl_wait();
+  pdl_trigger();
+  const PdlpState* st = V.st;
+  const int done = st->done;
+  const double sigma = st->sigma, refl = st->refl;
+  const double kk = (double)(st->k_inner + j_in_chunk);
+  double s[kSegPerLane], lo[kSegPerLane], hi[kSegPerLane];
+  seg_rows(op, tk, lane, V.xbar, s, lo, hi);
+  if (done) return;
+  const double lam = (kk + 1.0) / (kk + 2.0);
+  double dy = 0.0, dy0 = 0.0;
+#pragma unroll
+  for (int h = 0; h < kSegPerLane; ++h) {
+    const int i = lane + 32 * h;
+    if (i < cnt) {
+      const uint32_t r = first + i;
+      const double se = sigma * Ei[h];
+      const double yt = yi[h] - se * (s[h] - clampd(s[h] - yi[h] / se, lo[h], hi[h]));
+      V.y[r] = lam * ((1.0 + refl) * yt - refl * yi[h]) + (1.0 - lam) * y0[h];
+      if (CHECK) {
+        V.yt[r] = yt;
+        const double w = 1.0 / Ei[h];
+        dy += (yt - yi[h]) * (yt - yi[h]) * w;
+        dy0 += (yt - y0[h]) * (yt - y0[h]) * w;
+      }
+    }
+  }
+  if (CHECK) {
+    double a = block_sum(dy, sh);
+    if (threadIdx.x == 0) V.part[Q_DY * V.pstride + blockIdx.x] = a;
+    a = block_sum(dy0, sh);
+    if (threadIdx.x == 0) V.part[Q_DY0 * V.pstride + blockIdx.x] = a;
+  }
+}
+
 // KKT over rows at T(z) = (xt, yt): primal residual of A.xt against the row
 // bounds and the row part of the dual objective.
-template <bool UNIT>
-__global__ void __launch_bounds__(kThreads) kkt_row_kernel(int32_t m, SellView S, Vecs V) {
+template <bool UNIT, bool TE>
+__global__ void __launch_bounds__(kThreads) kkt_row_kernel(int32_t m, SellView S, TeOp op, Vecs V) {
   __shared__ double sh[32];
   if (V.st->done) return;
   const int64_t i = (int64_t)blockIdx.x * kTile + threadIdx.x;
-  const double s = (i < m) ? sell_dot<UNIT, 8>(S, i, V.xt) : 0.0;
+  double lo = 0.0, hi = 0.0, s = 0.0;
+  if (i < m) {
+    if (TE) {
+      s = te_row(op, (uint32_t)i, V.xt, lo, hi);
+    } else {
+      s = sell_dot<UNIT, 8>(S, i, V.xt);
+      lo = V.lo_u[i];
+      hi = V.hi_u[i];
+    }
+  }
   double rp = 0.0, dobj = 0.0;
   if (i < m) {
-    const double lo = V.lo_u[i], hi = V.hi_u[i];
     const double r = s - clampd(s, lo, hi);
     rp = r * r;
     const double yu = V.yt[i];
@@ -513,17 +736,25 @@ __global__ void __launch_bounds__(kThreads) kkt_row_kernel(int32_t m, SellView S
 
 // KKT over columns: reduced costs, dual residual, primal objective and the
 // bound part of the dual objective.
-template <bool UNIT>
-__global__ void __launch_bounds__(kThreads) kkt_col_kernel(int32_t n, SellView S, Vecs V) {
+template <bool UNIT, bool TE>
+__global__ void __launch_bounds__(kThreads) kkt_col_kernel(int32_t n, SellView S, TeOp op, Vecs V) {
   __shared__ double sh[32];
   if (V.st->done) return;
   const int64_t j = (int64_t)blockIdx.x * kTile + threadIdx.x;
-  const double s = (j < n) ? sell_dot<UNIT>(S, j, V.yt) : 0.0;
+  double lb = 0.0, ub = 0.0, cj = 0.0, s = 0.0;
+  if (j < n) {
+    if (TE) {
+      s = te_col(op, (uint32_t)j, V.yt, lb, ub, cj);
+    } else {
+      s = sell_dot<UNIT>(S, j, V.yt);
+      cj = V.c_u[j];
+      lb = V.lb_u[j];
+      ub = V.ub_u[j];
+    }
+  }
   double rd = 0.0, pobj = 0.0, dobj = 0.0;
   if (j < n) {
-    const double cj = V.c_u[j];
     const double g = cj - s;
-    const double lb = V.lb_u[j], ub = V.ub_u[j];
     double lamb = 0.0;
     if (g > 0.0 && isfinite(lb)) lamb = g;
     else if (g < 0.0 && isfinite(ub)) lamb = g;
@@ -939,18 +1170,47 @@ int pipe_blocks() {
   return blocks;
 }
 
+// Launch an iteration kernel, with programmatic stream serialization (PDL)
+// when `pdl` is set.
+template <typename... KArgs, typename... Args>
+void launch_iter(bool pdl, void (*k)(KArgs...), int grid, cudaStream_t st, Args... args) {
+  if (!pdl) {
+    k<<<grid, kThreads, 0, st>>>(args...);
+    return;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k, args...);
+}
+
 template <bool UNIT, bool DICT, bool CHECK>
-void launch_col(cudaStream_t st, const teccl_lp* lp, const Vecs& V, int j) {
-  if (V.col_pipe) {
+void launch_col(cudaStream_t st, const teccl_lp* lp, const TeOp* te, const Vecs& V, int j) {
+  const bool pdl = V.pdl != 0;
+  if (te && V.seg) {
+    launch_iter(pdl, col_seg_kernel<CHECK>, (te->n_ctask + 7) / 8, st, *te, V, j);
+  } else if (te) {
+    launch_iter(pdl, col_te_kernel<CHECK>, (int)((te->n + kTile - 1) / kTile), st, *te, V, j);
+  } else if (V.col_pipe) {
     const int blocks = std::min<int>(pipe_blocks(), V.nb_col);
-    col_pipe_kernel<UNIT, DICT, CHECK><<<blocks, kThreads, 0, st>>>(lp->n, col_view(lp), V, j);
+    launch_iter(pdl, col_pipe_kernel<UNIT, DICT, CHECK>, blocks, st, (int32_t)lp->n, col_view(lp), V, j);
   } else {
-    col_step_kernel<UNIT, DICT, CHECK><<<V.nb_col, kThreads, 0, st>>>(lp->n, col_view(lp), V, j);
+    launch_iter(pdl, col_step_kernel<UNIT, DICT, CHECK>, V.nb_col, st, (int32_t)lp->n, col_view(lp), V, j);
   }
 }
 template <bool UNIT, bool DICT, bool CHECK>
-void launch_row(cudaStream_t st, const teccl_lp* lp, const Vecs& V, int j) {
-  row_step_kernel<UNIT, DICT, CHECK><<<V.nb_row, kThreads, 0, st>>>(lp->m, row_view(lp), V, j);
+void launch_row(cudaStream_t st, const teccl_lp* lp, const TeOp* te, const Vecs& V, int j) {
+  const bool pdl = V.pdl != 0;
+  if (te && V.seg) launch_iter(pdl, row_seg_kernel<CHECK>, (te->n_rtask + 7) / 8, st, *te, V, j);
+  else if (te) launch_iter(pdl, row_te_kernel<CHECK>, (int)((te->m + kTile - 1) / kTile), st, *te, V, j);
+  else launch_iter(pdl, row_step_kernel<UNIT, DICT, CHECK>, V.nb_row, st, (int32_t)lp->m, row_view(lp), V, j);
 }
 
 struct StepBench {
@@ -983,22 +1243,27 @@ struct Exchange {
 };
 
 template <bool UNIT, bool DICT>
-void enqueue_chunk(int chunk, cudaStream_t st, const teccl_lp* lp, const Vecs& Vc, const Vecs& Vr,
+void enqueue_chunk(int chunk, cudaStream_t st, const teccl_lp* lp, const TeOp* te, const Vecs& Vc, const Vecs& Vr,
                    Exchange& X, double* y_w, double* yt_w) {
   const int64_t nrw = gather_rows(lp), orr = own_row_off(lp);
   for (int j = 0; j < chunk; ++j) {
     const bool check = (j == chunk - 1);
-    if (check) launch_col<UNIT, DICT, true>(st, lp, Vc, j);
-    else launch_col<UNIT, DICT, false>(st, lp, Vc, j);
+    if (check) launch_col<UNIT, DICT, true>(st, lp, te, Vc, j);
+    else launch_col<UNIT, DICT, false>(st, lp, te, Vc, j);
     if (check) X.halo(st, {A_XBAR, A_XT});
     else X.halo(st, {A_XBAR});
-    if (check) launch_row<UNIT, DICT, true>(st, lp, Vr, j);
-    else launch_row<UNIT, DICT, false>(st, lp, Vr, j);
+    if (check) launch_row<UNIT, DICT, true>(st, lp, te, Vr, j);
+    else launch_row<UNIT, DICT, false>(st, lp, te, Vr, j);
     if (check) X.halo(st, {A_Y, A_YT});
     else X.halo(st, {A_Y});
   }
-  kkt_row_kernel<UNIT><<<Vr.nb_row, kThreads, 0, st>>>(lp->m, row_view(lp), Vr);
-  kkt_col_kernel<UNIT><<<Vc.nb_col, kThreads, 0, st>>>(lp->n, col_view(lp), Vc);
+  if (te) {
+    kkt_row_kernel<UNIT, true><<<Vr.nb_row, kThreads, 0, st>>>(lp->m, SellView{}, *te, Vr);
+    kkt_col_kernel<UNIT, true><<<Vc.nb_col, kThreads, 0, st>>>(lp->n, SellView{}, *te, Vc);
+  } else {
+    kkt_row_kernel<UNIT, false><<<Vr.nb_row, kThreads, 0, st>>>(lp->m, row_view(lp), TeOp{}, Vr);
+    kkt_col_kernel<UNIT, false><<<Vc.nb_col, kThreads, 0, st>>>(lp->n, col_view(lp), TeOp{}, Vc);
+  }
   reduce_publish_kernel<<<1, 1024, 0, st>>>(Vc, X.active() ? X.ds->sig_all : Signal{},
                                             X.active() ? X.ds->d_peer_slots : nullptr);
   X.wait_all(st);
@@ -1043,6 +1308,10 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
     ws->st = st;
     Workspace& W = *ws;
     W.pstride = std::max<int64_t>(std::max(nb_row, nb_col), kGrid);
+    if (lp->te) {
+      const TeOp& t = ((TeHold*)lp->te)->op;
+      W.pstride = std::max<int64_t>(W.pstride, std::max((t.n_ctask + 7) / 8, (t.n_rtask + 7) / 8));
+    }
     W.rstat = W.alloc<double>(m); W.cstat = W.alloc<double>(n);
     W.D = W.alloc<float>(n); W.E = W.alloc<float>(m);
     W.x0 = W.alloc<float>(n); W.y0 = W.alloc<float>(m);
@@ -1103,7 +1372,13 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
   TECCL_CUDA(cudaMemsetAsync(xbar_w, 0, sizeof(double) * (ncw + 1), st));
   TECCL_CUDA(cudaMemsetAsync(y_w, 0, sizeof(double) * (nrw + 1), st));
   TECCL_CUDA(cudaMemsetAsync(yt_w, 0, sizeof(double) * (nrw + 1), st));
-  {
+  // matrix-free operator for single-device TE LPs; the SELL copies are
+  // only built for LPs that need them
+  const TeOp* te = (o->matrix_free && lp->te && lp->part_world == 1) ? &((TeHold*)lp->te)->op : nullptr;
+  // segment kernels unless per-entry is asked for (2) or the segments are
+  // too short to fill a warp task (auto, K < 16)
+  const bool seg = te && (o->matrix_free == 3 || (o->matrix_free == 1 && te->K >= 16));
+  if (!te) {
     int rc = teccl_build_sell(lp, st);
     if (rc) return rc;
   }
@@ -1237,6 +1512,14 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
   V.world = world;
   V.rank = rank;
   V.col_pipe = o->col_pipeline;
+  V.pdl = o->pdl;
+  V.seg = seg ? 1 : 0;
+  // partial-sum slots: the iteration kernels write one per block; the
+  // reduction reads max(blocks) slots per quantity (unwritten ones stay 0)
+  if (seg) {
+    V.nb_col = std::max(V.nb_col, (te->n_ctask + 7) / 8);
+    V.nb_row = std::max(V.nb_row, (te->n_rtask + 7) / 8);
+  }
   // Vc: column kernels (own x side, gather y windows); Vr: row kernels
   // (own y side, gather x windows); Vi: owned parts only
   Vecs Vc = V, Vr = V, Vi = V;
@@ -1254,13 +1537,13 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
     TECCL_CUDA(cudaEventCreate(&b));
     TECCL_CUDA(cudaEventCreate(&c2));
     for (int w = 0; w < 3; ++w) {
-      launch_col<UNIT, DICT, false>(st, lp, Vc, 0);
-      launch_row<UNIT, DICT, false>(st, lp, Vr, 0);
+      launch_col<UNIT, DICT, false>(st, lp, te, Vc, 0);
+      launch_row<UNIT, DICT, false>(st, lp, te, Vr, 0);
     }
     TECCL_CUDA(cudaEventRecord(a, st));
-    for (int r = 0; r < sb->reps; ++r) launch_col<UNIT, DICT, false>(st, lp, Vc, 0);
+    for (int r = 0; r < sb->reps; ++r) launch_col<UNIT, DICT, false>(st, lp, te, Vc, 0);
     TECCL_CUDA(cudaEventRecord(b, st));
-    for (int r = 0; r < sb->reps; ++r) launch_row<UNIT, DICT, false>(st, lp, Vr, 0);
+    for (int r = 0; r < sb->reps; ++r) launch_row<UNIT, DICT, false>(st, lp, te, Vr, 0);
     TECCL_CUDA(cudaEventRecord(c2, st));
     TECCL_CHECK_LAUNCH();
     TECCL_CUDA(cudaEventSynchronize(c2));
@@ -1271,6 +1554,12 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
     sb->ms_row = m2 / sb->reps;
     // algorithmic bytes: SELL slice headers and every
     // stored entry once, the gathered vector once, dense operands once
+    if (te) {  // no stored matrix: dense vectors, the gathered operand once, capacities
+      sb->bytes_col = 8.0 * nrw + 32.0 * n;
+      sb->bytes_row = 8.0 * ncw + 24.0 * m + 8.0 * (double)te->EK;
+      cudaEventDestroy(a); cudaEventDestroy(b); cudaEventDestroy(c2);
+      return TECCL_OK;
+    }
     const double ib = UNIT ? 4.0 : 12.0;
     const double ns_c = (double)((n + 31) / 32), ns_r = (double)((m + 31) / 32);
     const double cb = DICT ? 2.0 : 24.0, rbd = DICT ? 2.0 : 16.0;
@@ -1283,7 +1572,7 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
   }
 
   // --- chunk graph (captured once per LP and chunk length)
-  const int graph_key = chunk * 2 + (o->col_pipeline ? 1 : 0);
+  const int graph_key = chunk * 16 + (o->col_pipeline ? 1 : 0) + (te ? 2 : 0) + (o->pdl ? 4 : 0) + (seg ? 8 : 0);
   if (o->use_graphs && W.gexec && W.graph_chunk != graph_key) {
     cudaGraphExecDestroy(W.gexec);
     W.gexec = nullptr;
@@ -1296,7 +1585,7 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
     cudaStream_t cap;
     TECCL_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
     TECCL_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
-    enqueue_chunk<UNIT, DICT>(chunk, cap, lp, Vc, Vr, X, y_w, yt_w);
+    enqueue_chunk<UNIT, DICT>(chunk, cap, lp, te, Vc, Vr, X, y_w, yt_w);
     TECCL_CUDA(cudaStreamEndCapture(cap, &g));
     TECCL_CUDA(cudaGraphInstantiate(&W.gexec, g, 0));
     TECCL_CUDA(cudaGraphDestroy(g));
@@ -1332,7 +1621,7 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
       if (gexec) {
         TECCL_CUDA(cudaGraphLaunch(gexec, st));
       } else {
-        enqueue_chunk<UNIT, DICT>(chunk, st, lp, Vc, Vr, X, y_w, yt_w);
+        enqueue_chunk<UNIT, DICT>(chunk, st, lp, te, Vc, Vr, X, y_w, yt_w);
       }
       TECCL_CHECK_LAUNCH();
       const int slot = (int)(launched % look);
@@ -1425,6 +1714,8 @@ extern "C" void teccl_pdlp_default_opts(teccl_pdlp_opts* o) {
   o->omega_ki = 0.0;
   o->omega_kd = 0.0;
   o->col_pipeline = 1;
+  o->matrix_free = 0;  // measured: the SELL kernels are faster on configs[1] (profiles/r01_h)
+  o->pdl = 1;
 }
 
 extern "C" int teccl_pdlp_solve_dev(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* opts,
@@ -1478,9 +1769,89 @@ extern "C" int teccl_pdlp_step_bench(teccl_ctx* ctx, teccl_lp* lp, int32_t reps,
   cudaFreeAsync(xd, ctx->stream);
   TECCL_CUDA(cudaStreamSynchronize(ctx->stream));
   out6[0] = sb.ms_col; out6[1] = sb.ms_row; out6[2] = sb.bytes_col; out6[3] = sb.bytes_row;
-  out6[4] = (lp->col_code && lp->row_code) ? 1.0 : 0.0;  // bounds via class dictionaries
+  // operator: 2 matrix-free, 1 stored matrix + bound-class dictionaries, 0 stored + arrays
+  out6[4] = (o.matrix_free && lp->te && lp->part_world == 1) ? 2.0 : (lp->col_code && lp->row_code) ? 1.0 : 0.0;
   out6[5] = (double)kSlice;
   return rc;
+}
+
+namespace teccl {
+// out = A.in (rows) or A^T.in (columns) through the matrix-free operator,
+// with the bounds (and costs) that operator computes
+__global__ void te_apply_kernel(TeOp op, int transpose, const double* __restrict__ in,
+                                double* out, double* lo, double* hi, double* c) {
+  const uint32_t count = transpose ? op.n : op.m;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x) {
+    double a, b, cc = 0.0;
+    const double v = transpose ? te_col(op, i, in, a, b, cc) : te_row(op, i, in, a, b);
+    out[i] = v;
+    lo[i] = a;
+    hi[i] = b;
+    if (transpose) c[i] = cc;
+  }
+}
+
+__global__ void seg_apply_kernel(TeOp op, int transpose, const double* __restrict__ in,
+                                 double* out, double* lo, double* hi, double* c) {
+  const int wi = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  const int nt = transpose ? op.n_ctask : op.n_rtask;
+  if (wi >= nt) return;
+  const int4 tk = __ldg((transpose ? op.ctask : op.rtask) + wi);
+  double a[kSegPerLane], l[kSegPerLane], u[kSegPerLane], cc[kSegPerLane];
+  if (transpose) seg_cols(op, tk, lane, in, a, l, u, cc);
+  else seg_rows(op, tk, lane, in, a, l, u);
+  for (int h = 0; h < kSegPerLane; ++h) {
+    const int i = lane + 32 * h;
+    if (i < seg_count(tk)) {
+      const uint32_t r = (uint32_t)tk.z + i;
+      out[r] = a[h];
+      lo[r] = l[h];
+      hi[r] = u[h];
+      if (transpose) c[r] = cc[h];
+    }
+  }
+}
+}  // namespace teccl
+
+extern "C" int teccl_lp_apply(teccl_ctx* ctx, teccl_lp* lp, int32_t transpose, int32_t matrix_free,
+                              const double* in, double* out, double* lo, double* hi, double* cost) {
+  if (!ctx || !lp || !in || !out) { set_error("null argument"); return TECCL_EINVAL; }
+  if (matrix_free && !lp->te) { set_error("LP has no matrix-free operator (not built by teccl_lp_build_te)"); return TECCL_EINVAL; }
+  cudaStream_t st = ctx->stream;
+  TECCL_CUDA(cudaSetDevice(ctx->device));
+  const int64_t nin = transpose ? lp->m : lp->n, nout = transpose ? lp->n : lp->m;
+  double *din = nullptr, *dout = nullptr;
+  TECCL_CUDA(cudaMallocAsync((void**)&din, sizeof(double) * (nin + 1), st));
+  TECCL_CUDA(cudaMallocAsync((void**)&dout, sizeof(double) * 4 * (nout + 1), st));
+  TECCL_CUDA(cudaMemcpyAsync(din, in, sizeof(double) * nin, cudaMemcpyHostToDevice, st));
+  double *dlo = dout + (nout + 1), *dhi = dlo + (nout + 1), *dc = dhi + (nout + 1);
+  if (matrix_free == 2) {
+    const TeOp& op = ((TeHold*)lp->te)->op;
+    const int nt = transpose ? op.n_ctask : op.n_rtask;
+    seg_apply_kernel<<<(nt + 7) / 8, kThreads, 0, st>>>(op, transpose, din, dout, dlo, dhi, dc);
+  } else if (matrix_free) {
+    te_apply_kernel<<<grid_for(nout), kThreads, 0, st>>>(((TeHold*)lp->te)->op, transpose, din, dout, dlo, dhi, dc);
+  } else {
+    if (lp->unit) {
+      if (transpose) spmv_scaled_kernel<true><<<grid_for(nout), kThreads, 0, st>>>(nout, lp->col_ptr, lp->row, lp->cval, din, nullptr, dout);
+      else spmv_scaled_kernel<true><<<grid_for(nout), kThreads, 0, st>>>(nout, lp->row_ptr, lp->col, lp->val, din, nullptr, dout);
+    } else {
+      if (transpose) spmv_scaled_kernel<false><<<grid_for(nout), kThreads, 0, st>>>(nout, lp->col_ptr, lp->row, lp->cval, din, nullptr, dout);
+      else spmv_scaled_kernel<false><<<grid_for(nout), kThreads, 0, st>>>(nout, lp->row_ptr, lp->col, lp->val, din, nullptr, dout);
+    }
+    TECCL_CUDA(cudaMemcpyAsync(dlo, transpose ? lp->var_lb : lp->row_lo, sizeof(double) * nout, cudaMemcpyDeviceToDevice, st));
+    TECCL_CUDA(cudaMemcpyAsync(dhi, transpose ? lp->var_ub : lp->row_hi, sizeof(double) * nout, cudaMemcpyDeviceToDevice, st));
+    if (transpose) TECCL_CUDA(cudaMemcpyAsync(dc, lp->obj, sizeof(double) * nout, cudaMemcpyDeviceToDevice, st));
+  }
+  TECCL_CHECK_LAUNCH();
+  TECCL_CUDA(cudaMemcpyAsync(out, dout, sizeof(double) * nout, cudaMemcpyDeviceToHost, st));
+  if (lo) TECCL_CUDA(cudaMemcpyAsync(lo, dlo, sizeof(double) * nout, cudaMemcpyDeviceToHost, st));
+  if (hi) TECCL_CUDA(cudaMemcpyAsync(hi, dhi, sizeof(double) * nout, cudaMemcpyDeviceToHost, st));
+  if (cost && transpose) TECCL_CUDA(cudaMemcpyAsync(cost, dc, sizeof(double) * nout, cudaMemcpyDeviceToHost, st));
+  cudaFreeAsync(din, st);
+  cudaFreeAsync(dout, st);
+  TECCL_CUDA(cudaStreamSynchronize(st));
+  return TECCL_OK;
 }
 
 extern "C" int teccl_spmv_bench(teccl_ctx* ctx, teccl_lp* lp, int32_t reps, double* ms_per_pair,

@@ -20,55 +20,9 @@
 #include <vector>
 
 #include "common.cuh"
+#include "te_gen.cuh"
 
 namespace teccl {
-
-struct TeDev {
-  int Nn, E, S, P, K, G;
-  int64_t SB, CB, R_cons, R_cum, R_bcap, n_rows, n_vars;
-  int has_bcap;
-  double blimit;
-  const uint8_t* is_sw;
-  const int* gpu_of;     // [Nn] GPU rank or -1
-  const int* gpre;       // [Nn] GPUs strictly before node n
-  const int* node_of_gpu;// [G]
-  const int* esrc;
-  const int* edst;
-  const int* edelta;
-  const double* ecap;    // [E*K]
-  const int* snode;      // [S]
-  const int* pair_src;   // [P]
-  const int* pair_dst;   // [P]
-  const double* pair_u;  // [P]
-  const int* pair_of;    // [S*Nn] pair id or -1
-  const double* out_units;  // [S]
-  const int* inc_ptr;    // [Nn+1]
-  const uint32_t* inc;   // edge id | bit31 when the edge leaves the node
-  const int* out_ptr;    // [Nn+1] out-edges of node (edge order)
-  const int* out_e;
-  // bound-class codes (pdlp.cu dictionaries)
-  int dict_col, dict_row, nU, nOU, nCap;
-  int phase1;
-  const int* pair_uidx;  // [P] index of the pair's units in the distinct-units list
-  const int* src_ouidx;  // [S] index of the source's out-units in its list
-  const uint16_t* cap_idx;  // [E*K] index of the capacity in the distinct-caps list
-};
-
-__device__ __forceinline__ int64_t varF(const TeDev& d, int s, int e, int k) {
-  return (int64_t)s * d.SB + (int64_t)e * d.K + k;
-}
-__device__ __forceinline__ int64_t varB(const TeDev& d, int s, int g, int k) {
-  return (int64_t)s * d.SB + (int64_t)d.E * d.K + (int64_t)g * (d.K + 1) + k;
-}
-__device__ __forceinline__ int64_t varRd(const TeDev& d, int p, int k) {
-  return (int64_t)d.S * d.SB + (int64_t)p * 2 * d.K + 2 * k;
-}
-__device__ __forceinline__ int64_t cons_off(const TeDev& d, int s, int n) {
-  return (int64_t)n * d.K + d.gpre[n] - (d.snode[s] < n ? 1 : 0);
-}
-__device__ __forceinline__ int64_t rowCons(const TeDev& d, int s, int n, int k) {
-  return d.R_cons + (int64_t)s * d.CB + cons_off(d, s, n) + k;
-}
 
 // Emit helper: count or write one (index, sign) entry.
 template <bool FILL>
@@ -697,6 +651,86 @@ int setup_dicts(const teccl_te_desc* desc, TeDev& d, teccl_lp* lp, std::vector<v
 
 }  // namespace
 
+namespace {
+// packed tables of the matrix-free operator (TeOp in te_gen.cuh)
+int te_op_tables(const teccl_te_desc* desc, TeHold* h, cudaStream_t st) {
+  TeOp& o = h->op;
+  const int Nn = desc->num_nodes, E = desc->num_edges, S = desc->num_sources, P = desc->num_pairs;
+  const int64_t K = desc->K;
+  std::vector<int> gpre(Nn, 0);
+  for (int n = 0, g = 0; n < Nn; ++n) { gpre[n] = g; if (!desc->node_is_switch[n]) ++g; }
+  std::vector<int4> edge4(E);
+  for (int e = 0; e < E; ++e) edge4[e] = make_int4(desc->edge_src[e], desc->edge_dst[e], desc->edge_delta[e], 0);
+  std::vector<int2> sntab((size_t)S * Nn);
+  for (int s = 0; s < S; ++s)
+    for (int n = 0; n < Nn; ++n) {
+      const int sn = desc->source_node[s];
+      const int64_t first = (int64_t)o.R_cons + (int64_t)s * o.CB + (int64_t)n * K + gpre[n] - (sn < n ? 1 : 0);
+      const bool has_last = !desc->node_is_switch[n] && n != sn;
+      sntab[(size_t)s * Nn + n] = make_int2((int)((uint32_t)first | (has_last ? kSignBit : 0u)), -1);
+    }
+  for (int p = 0; p < P; ++p)
+    sntab[(size_t)desc->pair_source[p] * Nn + desc->pair_dst[p]].y = (int)(o.nF + (int64_t)p * 2 * K);
+  // incident entries in the builder's order: per node, edges ascending, each
+  // edge once as leaving (at its source) and once as arriving (at its dst)
+  std::vector<int> cnt(Nn + 1, 0);
+  for (int e = 0; e < E; ++e) { cnt[desc->edge_src[e] + 1]++; cnt[desc->edge_dst[e] + 1]++; }
+  for (int n = 0; n < Nn; ++n) cnt[n + 1] += cnt[n];
+  std::vector<int2> incp(cnt[Nn]);
+  {
+    std::vector<int> fill(cnt.begin(), cnt.end() - 1);
+    for (int e = 0; e < E; ++e) {
+      incp[fill[desc->edge_src[e]]++] = make_int2((int)(e * K + 1), -1);
+      incp[fill[desc->edge_dst[e]]++] = make_int2((int)(e * K - desc->edge_delta[e]), desc->edge_delta[e]);
+    }
+  }
+  // segment tasks, in memory order (seg_cols / seg_rows in te_gen.cuh)
+  std::vector<int4> ct, rt;
+  auto add = [](std::vector<int4>& v, int kind, int a, int b, int64_t start, int64_t len) {
+    for (int64_t off = 0; off < len; off += kSegTask) {
+      const int cnt = (int)std::min<int64_t>(kSegTask, len - off);
+      v.push_back(make_int4(kind | (a << 4), b, (int)(start + off), (int)(off | ((int64_t)cnt << 24))));
+    }
+  };
+  const int G = (int)(o.SB - (int64_t)E * K) / (int)(K + 1);
+  for (int s = 0; s < S; ++s) {
+    for (int e = 0; e < E; ++e) add(ct, SEG_F, s, e, (int64_t)s * o.SB + (int64_t)e * K, K);
+    for (int g = 0; g < G; ++g) add(ct, SEG_B, s, g, (int64_t)s * o.SB + o.EK + (int64_t)g * (K + 1), K + 1);
+  }
+  for (int p = 0; p < P; ++p) add(ct, SEG_P, p, 0, (int64_t)o.nF + (int64_t)p * 2 * K, 2 * K);
+  add(rt, SEG_INIT, 0, 0, 0, S);
+  for (int e = 0; e < E; ++e) add(rt, SEG_CAP, 0, e, (int64_t)S + (int64_t)e * K, K);
+  for (int s = 0; s < S; ++s)
+    for (int n = 0; n < Nn; ++n) {
+      const uint32_t f = (uint32_t)sntab[(size_t)s * Nn + n].x;
+      add(rt, SEG_CONS, s, n, f & kIdxMask, K + ((f & kSignBit) ? 1 : 0));
+    }
+  for (int p = 0; p < P; ++p) add(rt, SEG_CUM, p, 0, (int64_t)o.R_cum + (int64_t)p * K, K);
+  if (o.has_bcap)
+    for (int g = 0; g < G; ++g) add(rt, SEG_BCAP, 0, g, (int64_t)o.R_bcap + (int64_t)g * (K + 1), K + 1);
+  std::vector<double> ninv(K);
+  for (int64_t k = 0; k < K; ++k) ninv[k] = -1.0 / (double)(k + 1);
+  int4* d4 = nullptr; int2* ds = nullptr; int2* di = nullptr;
+  int4 *dct = nullptr, *drt = nullptr;
+  double* dni = nullptr;
+  if (upload(edge4, &d4, st) || upload(sntab, &ds, st) || upload(incp, &di, st) ||
+      upload(ct, &dct, st) || upload(rt, &drt, st) || upload(ninv, &dni, st))
+    return TECCL_ECUDA;
+  for (void* p : {(void*)d4, (void*)ds, (void*)di, (void*)dct, (void*)drt, (void*)dni}) h->owned.push_back(p);
+  o.edge4 = d4; o.sntab = ds; o.incp = di;
+  o.ctask = dct; o.rtask = drt; o.neg_inv = dni;
+  o.n_ctask = (int)ct.size(); o.n_rtask = (int)rt.size();
+  return TECCL_OK;
+}
+
+void free_te_hold(void* p) {
+  TeHold* h = (TeHold*)p;
+  for (void* q : h->owned) cudaFreeAsync(q, h->st);
+  cudaStreamSynchronize(h->st);
+  delete h;
+}
+}  // namespace
+
 extern "C" int teccl_lp_build_te(teccl_ctx* ctx, const teccl_te_desc* desc, teccl_lp** out) {
   if (!ctx || !desc || !out) { set_error("null argument"); return TECCL_EINVAL; }
   TeDev d;
@@ -764,7 +798,14 @@ extern "C" int teccl_lp_build_te(teccl_ctx* ctx, const teccl_te_desc* desc, tecc
   }
   TECCL_CUDA(cudaFreeAsync(row_len, st));
   TECCL_CUDA(cudaFreeAsync(col_len, st));
-  for (void* p : owned) TECCL_CUDA(cudaFreeAsync(p, st));
+  // keep the tables: the PDLP kernels apply A / A^T from them (matrix-free)
+  TeHold* h = new TeHold();
+  te_op_init(h->op, d);
+  h->owned.swap(owned);
+  h->st = st;
+  if (int rc = te_op_tables(desc, h, st)) { free_te_hold(h); return rc; }
+  lp->te = h;
+  lp->te_free = free_te_hold;
   TECCL_CUDA(cudaStreamSynchronize(st));
   *out = lp;
   return TECCL_OK;

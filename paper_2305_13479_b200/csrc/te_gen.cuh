@@ -1,0 +1,485 @@
+// Time-expanded LP structure shared by the builder (te_build.cu) and the
+// PDLP iteration kernels (pdlp.cu).
+//
+// TeDev holds the small per-node / per-edge / per-pair tables the copy-free
+// TE-CCL LP (reference pkg/src/collsched/lp.py:22-136) is generated from.
+// TeOp adds 32-bit invariant-divisor constants so the iteration kernels can
+// apply A and A^T straight from those tables ("matrix-free"): every entry is
+// +-1 and its row/column index is a closed form in (source, edge/GPU/pair,
+// epoch), so no index stream is read from HBM at all.
+#pragma once
+
+#include <cmath>
+#include <vector>
+
+#include "common.cuh"
+
+namespace teccl {
+
+struct TeDev {
+  int Nn, E, S, P, K, G;
+  int64_t SB, CB, R_cons, R_cum, R_bcap, n_rows, n_vars;
+  int has_bcap;
+  double blimit;
+  const uint8_t* is_sw;
+  const int* gpu_of;     // [Nn] GPU rank or -1
+  const int* gpre;       // [Nn] GPUs strictly before node n
+  const int* node_of_gpu;// [G]
+  const int* esrc;
+  const int* edst;
+  const int* edelta;
+  const double* ecap;    // [E*K]
+  const int* snode;      // [S]
+  const int* pair_src;   // [P]
+  const int* pair_dst;   // [P]
+  const double* pair_u;  // [P]
+  const int* pair_of;    // [S*Nn] pair id or -1
+  const double* out_units;  // [S]
+  const int* inc_ptr;    // [Nn+1]
+  const uint32_t* inc;   // edge id | bit31 when the edge leaves the node
+  const int* out_ptr;    // [Nn+1] out-edges of node (edge order)
+  const int* out_e;
+  // bound-class codes (pdlp.cu dictionaries)
+  int dict_col, dict_row, nU, nOU, nCap;
+  int phase1;
+  const int* pair_uidx;  // [P] index of the pair's units in the distinct-units list
+  const int* src_ouidx;  // [S] index of the source's out-units in its list
+  const uint16_t* cap_idx;  // [E*K] index of the capacity in the distinct-caps list
+};
+
+__device__ __forceinline__ int64_t varF(const TeDev& d, int s, int e, int k) {
+  return (int64_t)s * d.SB + (int64_t)e * d.K + k;
+}
+__device__ __forceinline__ int64_t varB(const TeDev& d, int s, int g, int k) {
+  return (int64_t)s * d.SB + (int64_t)d.E * d.K + (int64_t)g * (d.K + 1) + k;
+}
+__device__ __forceinline__ int64_t varRd(const TeDev& d, int p, int k) {
+  return (int64_t)d.S * d.SB + (int64_t)p * 2 * d.K + 2 * k;
+}
+__device__ __forceinline__ int64_t cons_off(const TeDev& d, int s, int n) {
+  return (int64_t)n * d.K + d.gpre[n] - (d.snode[s] < n ? 1 : 0);
+}
+__device__ __forceinline__ int64_t rowCons(const TeDev& d, int s, int n, int k) {
+  return d.R_cons + (int64_t)s * d.CB + cons_off(d, s, n) + k;
+}
+
+
+// ---------------------------------------------------------------------------
+// Division by a run-time invariant d for dividends < 2^31 (multiply-high and
+// shift; d = 1 is the identity).
+struct FastDiv {
+  uint32_t mul = 0, shr = 0;
+  void init(uint32_t d) {
+    if (d <= 1) { mul = 0; shr = 0; return; }
+    uint32_t l = 0;
+    while ((1ull << l) < d) ++l;                   // ceil(log2 d)
+    const uint32_t p = 31 + l;
+    mul = (uint32_t)(((1ull << p) + d - 1) / d);
+    shr = p - 32;
+  }
+  __device__ __forceinline__ uint32_t div(uint32_t n) const {
+    return mul ? (__umulhi(n, mul) >> shr) : n;
+  }
+};
+
+// Matrix-free view of a single-device TE LP (reference numbering; every
+// index < 2^31, checked by teccl_lp_build_te). The packed tables shorten the
+// chain of dependent table loads in front of each gather:
+//   edge4[e]        = {src, dst, delta, 0}
+//   sntab[s*Nn + n] = {first cons row of (s, n) | bit31 when (s, n) has a
+//                      "last" row, Rd(p, 0) column of pair (s, n) or -1}
+//   incp[j]         = incident entry j of node n (inc_ptr order):
+//                     {e*K - d, d}, d = delay for an arriving edge (term
+//                     +F(s,e,k-d)), d = -1 for a leaving edge (term -F(s,e,k+1))
+struct TeOp {
+  TeDev d;
+  FastDiv fK, fK1, f2K, fSB, fCB;
+  uint32_t K, S, Nn, SB, CB, EK, nF, R_cons, R_cum, R_bcap, m, n;
+  int has_bcap, phase1;
+  const int4* edge4;
+  const int2* sntab;
+  const int2* incp;
+  // segment tasks (see seg_cols / seg_rows): one warp per task
+  const int4* ctask;
+  const int4* rtask;
+  int n_ctask, n_rtask;
+  const double* neg_inv;   // [K] -1/(k+1), the Rc costs (lp.py:133-135)
+};
+
+// Owner of the device tables behind a TeOp (lp->te).
+struct TeHold {
+  TeOp op;
+  std::vector<void*> owned;
+  cudaStream_t st = nullptr;
+};
+
+inline void te_op_init(TeOp& o, const TeDev& d) {
+  o.d = d;
+  o.K = (uint32_t)d.K; o.S = (uint32_t)d.S; o.Nn = (uint32_t)d.Nn;
+  o.SB = (uint32_t)d.SB; o.CB = (uint32_t)d.CB;
+  o.EK = (uint32_t)((int64_t)d.E * d.K);
+  o.nF = (uint32_t)((int64_t)d.S * d.SB);
+  o.R_cons = (uint32_t)d.R_cons; o.R_cum = (uint32_t)d.R_cum; o.R_bcap = (uint32_t)d.R_bcap;
+  o.m = (uint32_t)d.n_rows; o.n = (uint32_t)d.n_vars;
+  o.has_bcap = d.has_bcap; o.phase1 = d.phase1;
+  o.fK.init(o.K); o.fK1.init(o.K + 1); o.f2K.init(2 * o.K);
+  o.fSB.init(o.SB > 0 ? o.SB : 1); o.fCB.init(o.CB > 0 ? o.CB : 1);
+  o.edge4 = nullptr; o.sntab = nullptr; o.incp = nullptr;
+  o.ctask = nullptr; o.rtask = nullptr; o.n_ctask = 0; o.n_rtask = 0; o.neg_inv = nullptr;
+}
+
+// (A^T y)_v for column v, with its bounds and cost (gen_col in te_build.cu
+// emits the same entries).
+__device__ __forceinline__ double te_col(const TeOp& o, uint32_t v, const double* __restrict__ y,
+                                         double& lb, double& ub, double& c) {
+  const uint32_t K = o.K;
+  lb = 0.0; ub = INFINITY; c = 0.0;
+  double a;
+  if (v < o.nF) {
+    const uint32_t s = o.fSB.div(v);
+    uint32_t q = v - s * o.SB;
+    const int sn = __ldg(o.d.snode + s);
+    const int2* sr = o.sntab + s * o.Nn;
+    if (q < o.EK) {                                // F(s,e,k)
+      const uint32_t e = o.fK.div(q), k = q - e * K;
+      const int4 ed = __ldg(o.edge4 + e);
+      const uint32_t cu = (uint32_t)__ldg(&sr[ed.x].x) & kIdxMask;
+      const uint32_t cw = (uint32_t)__ldg(&sr[ed.y].x);
+      const uint32_t t = k + (uint32_t)ed.z;
+      const double v_cap = __ldg(y + o.S + q);                                  // cap(e,k)
+      const double v_ini = (k == 0 && ed.x == sn) ? __ldg(y + s) : 0.0;         // init(s)
+      const double v_out = (k >= 1) ? __ldg(y + cu + k - 1) : 0.0;              // cons(s,u,k-1)
+      const double v_in = (t <= K - 1) ? __ldg(y + (cw & kIdxMask) + t) : 0.0;  // cons(s,w,t)
+      const double v_last = (t == K - 1 && (cw & kSignBit)) ? __ldg(y + (cw & kIdxMask) + K) : 0.0;
+      if (k == 0 && ed.x != sn) ub = 0.0;          // lp.py:51-52
+      a = v_cap + v_ini - v_out + v_in + v_last;
+    } else {                                       // B(s,g,k)
+      q -= o.EK;
+      const uint32_t g = o.fK1.div(q), k = q - g * (K + 1);
+      const int nd = __ldg(o.d.node_of_gpu + g);
+      const uint32_t rb = (uint32_t)__ldg(&sr[nd].x) & kIdxMask;
+      const double v_ini = (k == 0 && nd == sn) ? __ldg(y + s) : 0.0;
+      const double v_prev = (k >= 1) ? __ldg(y + rb + k - 1) : 0.0;
+      const double v_cur = (k <= K - 1) ? __ldg(y + rb + k) : 0.0;
+      const double v_bc = o.has_bcap ? __ldg(y + o.R_bcap + q) : 0.0;
+      if (k == 0 && nd != sn) ub = 0.0;            // lp.py:57-59
+      a = v_ini - v_prev + v_cur + v_bc;
+    }
+  } else {                                         // Rd(p,k) / Rc(p,k)
+    const uint32_t q = v - o.nF;
+    const uint32_t p = o.f2K.div(q), r = q - p * 2 * K, k = r >> 1;
+    const uint32_t cum = o.R_cum + p * K + k;
+    const double u = __ldg(o.d.pair_u + p);
+    ub = u;
+    if (!(r & 1)) {                                // Rd
+      const int s = __ldg(o.d.pair_src + p), w = __ldg(o.d.pair_dst + p);
+      const uint32_t rw = ((uint32_t)__ldg(&o.sntab[s * o.Nn + w].x) & kIdxMask) + k;
+      const double v_last = (k == K - 1) ? __ldg(y + rw + 1) : 0.0;
+      a = -__ldg(y + rw) - __ldg(y + cum) - v_last;
+    } else {                                       // Rc
+      const double v_next = (k + 1 <= K - 1) ? __ldg(y + cum + 1) : 0.0;
+      a = __ldg(y + cum) - v_next;
+      if (o.phase1) {
+        c = (k == K - 1) ? -1.0 : 0.0;
+      } else {
+        if (k == K - 1) lb = u;                    // lp.py:64-65
+        c = -1.0 / (double)(k + 1);                // lp.py:133-135
+      }
+    }
+  }
+  return a;
+}
+
+// sum over s < S of x[s*SB + off], loads issued 8 at a time
+__device__ __forceinline__ double te_sum_sources(const TeOp& o, const double* __restrict__ x, uint32_t off) {
+  double a = 0.0;
+  for (uint32_t s0 = 0; s0 < o.S; s0 += 8) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = (s0 + u < o.S) ? __ldg(x + (s0 + u) * o.SB + off) : 0.0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) a += v[u];
+  }
+  return a;
+}
+
+// (A x)_i for row i, with its bounds (gen_row in te_build.cu emits the same
+// entries).
+__device__ __forceinline__ double te_row(const TeOp& o, uint32_t i, const double* __restrict__ x,
+                                         double& lo, double& hi) {
+  const uint32_t K = o.K;
+  lo = 0.0; hi = 0.0;
+  double a = 0.0;
+  if (i < o.S) {                                   // init(s)
+    const int nd = __ldg(o.d.snode + i);
+    const double* xs = x + i * o.SB;
+    for (int j = __ldg(o.d.out_ptr + nd); j < __ldg(o.d.out_ptr + nd + 1); ++j)
+      a += __ldg(xs + (uint32_t)__ldg(o.d.out_e + j) * K);
+    a += __ldg(xs + o.EK + (uint32_t)__ldg(o.d.gpu_of + nd) * (K + 1));
+    lo = hi = __ldg(o.d.out_units + i);
+  } else if (i < o.R_cons) {                       // cap(e,k)
+    const uint32_t q = i - o.S;
+    a = te_sum_sources(o, x, q);
+    lo = -INFINITY;
+    hi = __ldg(o.d.ecap + q);
+  } else if (i < o.R_cum) {                        // cons(s,n,k) / last(s,n)
+    const uint32_t q = i - o.R_cons;
+    const uint32_t s = o.fCB.div(q);
+    const int2* sr = o.sntab + s * o.Nn;
+    const uint32_t base = o.R_cons + s * o.CB;
+    const uint32_t off = q - s * o.CB;
+    int nd = (int)o.fK1.div(off);                  // <= the node: offsets grow by K or K+1
+    int2 tn = __ldg(sr + nd);
+    while (nd + 1 < (int)o.Nn) {
+      const int2 tq = __ldg(sr + nd + 1);
+      if ((((uint32_t)tq.x & kIdxMask) - base) > off) break;
+      ++nd;
+      tn = tq;
+    }
+    const uint32_t k = off - (((uint32_t)tn.x & kIdxMask) - base);
+    const bool last = (k == K);
+    const int ke = last ? (int)K - 1 : (int)k;
+    const double* xs = x + s * o.SB;
+    const int j0 = __ldg(o.d.inc_ptr + nd), j1 = __ldg(o.d.inc_ptr + nd + 1);
+    for (int jb = j0; jb < j1; jb += 8) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        v[u] = 0.0;
+        if (jb + u < j1) {
+          const int2 t = __ldg(o.incp + jb + u);
+          const int kk = ke - t.y;
+          if (kk >= 0 && kk <= (int)K - 1 && !(last && t.y < 0)) {
+            const double xv = __ldg(xs + t.x + ke);
+            v[u] = t.y < 0 ? -xv : xv;
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) a += v[u];
+    }
+    const int g = __ldg(o.d.gpu_of + nd);
+    if (!last) {
+      if (g >= 0) {
+        const double* b = xs + o.EK + (uint32_t)g * (K + 1) + k;
+        a += __ldg(b) - __ldg(b + 1);
+        if (tn.y >= 0) a -= __ldg(x + (uint32_t)tn.y + 2 * k);
+      }
+    } else if (tn.y >= 0) {
+      a -= __ldg(x + (uint32_t)tn.y + 2 * (K - 1));
+    }
+  } else if (i < o.R_bcap) {                       // cum(p,k)
+    const uint32_t q = i - o.R_cum;
+    const uint32_t p = o.fK.div(q), k = q - p * K;
+    const uint32_t rd = o.nF + p * 2 * K + 2 * k;
+    const double v_prev = (k >= 1) ? __ldg(x + rd - 1) : 0.0;
+    a = __ldg(x + rd + 1) - __ldg(x + rd) - v_prev;
+  } else {                                         // bcap(g,k)
+    const uint32_t q = i - o.R_bcap;
+    a = te_sum_sources(o, x, o.EK + q);
+    lo = -INFINITY;
+    hi = o.d.blimit;
+  }
+  return a;
+}
+
+
+// ---------------------------------------------------------------------------
+// Segment walkers. Every column family is a run of consecutive epochs of one
+// (source, edge) / (source, GPU) / pair, and every row family a run of one
+// edge / (source, node) / pair / GPU, laid out contiguously. A task is up to
+// 64 consecutive entries of one segment, handled by one warp (entry
+// off + lane and off + 32 + lane): the segment's table lookups are done once
+// per task, each entry costs only its gathers, which are coalesced along the
+// epoch axis. Task encoding (int4):
+//   x = kind | a << 4,  y = b,  z = first global index of the task,
+//   w = off | count << 24   (off = epoch offset inside the segment)
+enum SegKind { SEG_F = 0, SEG_B = 1, SEG_P = 2,                          // columns
+               SEG_INIT = 3, SEG_CAP = 4, SEG_CONS = 5, SEG_CUM = 6, SEG_BCAP = 7 };  // rows
+constexpr int kSegPerLane = 2;
+constexpr int kSegTask = 32 * kSegPerLane;
+
+__device__ __forceinline__ int seg_count(const int4& t) { return (int)((uint32_t)t.w >> 24); }
+
+// (A^T y) for the task's entries lane + 32h, with bounds and costs.
+__device__ __forceinline__ void seg_cols(const TeOp& o, const int4& t, int lane,
+                                         const double* __restrict__ y, double (&a)[kSegPerLane],
+                                         double (&lb)[kSegPerLane], double (&ub)[kSegPerLane],
+                                         double (&c)[kSegPerLane]) {
+  const uint32_t K = o.K;
+  const int kind = t.x & 15, A = t.x >> 4, Bv = t.y;
+  const int off = t.w & 0xffffff, cnt = seg_count(t);
+#pragma unroll
+  for (int h = 0; h < kSegPerLane; ++h) { a[h] = 0.0; lb[h] = 0.0; ub[h] = INFINITY; c[h] = 0.0; }
+  if (kind == SEG_F) {                             // F(s,e,k), k = off + i
+    const int s = A, sn = __ldg(o.d.snode + s);
+    const int4 ed = __ldg(o.edge4 + Bv);
+    const int2* sr = o.sntab + s * o.Nn;
+    const uint32_t cu = (uint32_t)__ldg(&sr[ed.x].x) & kIdxMask;
+    const uint32_t cwr = (uint32_t)__ldg(&sr[ed.y].x);
+    const uint32_t cw = cwr & kIdxMask;
+    const bool wl = (cwr & kSignBit) != 0, from_src = (ed.x == sn);
+    const double* yc = y + o.S + (uint32_t)Bv * K;
+#pragma unroll
+    for (int h = 0; h < kSegPerLane; ++h) {
+      const int i = lane + 32 * h;
+      if (i < cnt) {
+        const uint32_t k = off + i, tt = k + (uint32_t)ed.z;
+        const double v_cap = __ldg(yc + k);
+        const double v_ini = (k == 0 && from_src) ? __ldg(y + s) : 0.0;
+        const double v_out = (k >= 1) ? __ldg(y + cu + k - 1) : 0.0;
+        const double v_in = (tt <= K - 1) ? __ldg(y + cw + tt) : 0.0;
+        const double v_last = (tt == K - 1 && wl) ? __ldg(y + cw + K) : 0.0;
+        a[h] = v_cap + v_ini - v_out + v_in + v_last;
+        if (k == 0 && !from_src) ub[h] = 0.0;      // lp.py:51-52
+      }
+    }
+  } else if (kind == SEG_B) {                      // B(s,g,k), k = off + i
+    const int s = A, g = Bv, sn = __ldg(o.d.snode + s);
+    const int nd = __ldg(o.d.node_of_gpu + g);
+    const uint32_t rb = (uint32_t)__ldg(&o.sntab[s * o.Nn + nd].x) & kIdxMask;
+    const bool at_src = (nd == sn);
+    const uint32_t bc = o.R_bcap + (uint32_t)g * (K + 1);
+#pragma unroll
+    for (int h = 0; h < kSegPerLane; ++h) {
+      const int i = lane + 32 * h;
+      if (i < cnt) {
+        const uint32_t k = off + i;
+        const double v_ini = (k == 0 && at_src) ? __ldg(y + s) : 0.0;
+        const double v_prev = (k >= 1) ? __ldg(y + rb + k - 1) : 0.0;
+        const double v_cur = (k <= K - 1) ? __ldg(y + rb + k) : 0.0;
+        const double v_bc = o.has_bcap ? __ldg(y + bc + k) : 0.0;
+        a[h] = v_ini - v_prev + v_cur + v_bc;
+        if (k == 0 && !at_src) ub[h] = 0.0;        // lp.py:57-59
+      }
+    }
+  } else if (kind == SEG_P) {                      // Rd/Rc(p,k), entry c = off + i = 2k + rc
+    const int p = A;
+    const int s = __ldg(o.d.pair_src + p), w = __ldg(o.d.pair_dst + p);
+    const uint32_t rw = (uint32_t)__ldg(&o.sntab[s * o.Nn + w].x) & kIdxMask;
+    const uint32_t cum = o.R_cum + (uint32_t)p * K;
+    const double u = __ldg(o.d.pair_u + p);
+#pragma unroll
+    for (int h = 0; h < kSegPerLane; ++h) {
+      const int i = lane + 32 * h;
+      if (i < cnt) {
+        const uint32_t cc = off + i, k = cc >> 1;
+        const bool rc = (cc & 1) != 0;
+        // Rd: -cons(s,w,k) - cum(p,k) [- last(s,w) at k = K-1];  Rc: cum(p,k) [- cum(p,k+1)]
+        const uint32_t i0 = rc ? cum + k : rw + k;
+        const double v0 = __ldg(y + i0);
+        const double v1 = rc ? ((k + 1 <= K - 1) ? __ldg(y + cum + k + 1) : 0.0) : __ldg(y + cum + k);
+        const double v2 = (!rc && k == K - 1) ? __ldg(y + rw + K) : 0.0;
+        a[h] = rc ? v0 - v1 : -v0 - v1 - v2;
+        ub[h] = u;
+        if (rc) {
+          if (o.phase1) {
+            c[h] = (k == K - 1) ? -1.0 : 0.0;
+          } else {
+            if (k == K - 1) lb[h] = u;             // lp.py:64-65
+            c[h] = __ldg(o.neg_inv + k);           // -1/(k+1), lp.py:133-135
+          }
+        }
+      }
+    }
+  }
+}
+
+// (A x) for the task's entries lane + 32h, with row bounds.
+__device__ __forceinline__ void seg_rows(const TeOp& o, const int4& t, int lane,
+                                         const double* __restrict__ x, double (&a)[kSegPerLane],
+                                         double (&lo)[kSegPerLane], double (&hi)[kSegPerLane]) {
+  const uint32_t K = o.K;
+  const int kind = t.x & 15, A = t.x >> 4, Bv = t.y;
+  const int off = t.w & 0xffffff, cnt = seg_count(t);
+#pragma unroll
+  for (int h = 0; h < kSegPerLane; ++h) { a[h] = 0.0; lo[h] = 0.0; hi[h] = 0.0; }
+  if (kind == SEG_CAP) {                           // cap(e,k): sum_s F(s,e,k)
+    const uint32_t q0 = (uint32_t)Bv * K + off;
+#pragma unroll
+    for (int h = 0; h < kSegPerLane; ++h) {
+      const int i = lane + 32 * h;
+      if (i < cnt) {
+        a[h] = te_sum_sources(o, x, q0 + i);
+        lo[h] = -INFINITY;
+        hi[h] = __ldg(o.d.ecap + q0 + i);
+      }
+    }
+  } else if (kind == SEG_CONS) {                   // cons(s,n,k) / last(s,n), k = off + i
+    const int s = A, nd = Bv;
+    const int2 tn = __ldg(o.sntab + s * o.Nn + nd);
+    const int g = __ldg(o.d.gpu_of + nd);
+    const int j0 = __ldg(o.d.inc_ptr + nd), j1 = __ldg(o.d.inc_ptr + nd + 1);
+    const double* xs = x + s * o.SB;
+    int kk[kSegPerLane];
+    bool last[kSegPerLane], on[kSegPerLane];
+#pragma unroll
+    for (int h = 0; h < kSegPerLane; ++h) {
+      const int i = lane + 32 * h;
+      on[h] = i < cnt;
+      const int k = off + i;
+      last[h] = (k == (int)K);
+      kk[h] = last[h] ? (int)K - 1 : k;
+    }
+    for (int jb = j0; jb < j1; jb += 4) {
+      int2 e4[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) e4[u] = (jb + u < j1) ? __ldg(o.incp + jb + u) : make_int2(0, (int)K);
+#pragma unroll
+      for (int h = 0; h < kSegPerLane; ++h) {
+        double v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int ke = kk[h] - e4[u].y;          // epoch of the term; out of range = absent
+          const bool ok = on[h] && ke >= 0 && ke <= (int)K - 1 && !(last[h] && e4[u].y < 0);
+          v[u] = ok ? __ldg(xs + e4[u].x + kk[h]) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) a[h] += (e4[u].y < 0) ? -v[u] : v[u];
+      }
+    }
+    const double* bg = xs + o.EK + (uint32_t)(g >= 0 ? g : 0) * (K + 1);
+#pragma unroll
+    for (int h = 0; h < kSegPerLane; ++h) {
+      if (!on[h]) continue;
+      if (!last[h]) {
+        if (g >= 0) {
+          a[h] += __ldg(bg + kk[h]) - __ldg(bg + kk[h] + 1);
+          if (tn.y >= 0) a[h] -= __ldg(x + (uint32_t)tn.y + 2 * kk[h]);
+        }
+      } else if (tn.y >= 0) {
+        a[h] -= __ldg(x + (uint32_t)tn.y + 2 * (K - 1));
+      }
+    }
+  } else if (kind == SEG_CUM) {                    // cum(p,k)
+    const uint32_t rd0 = o.nF + (uint32_t)A * 2 * K;
+#pragma unroll
+    for (int h = 0; h < kSegPerLane; ++h) {
+      const int i = lane + 32 * h;
+      if (i < cnt) {
+        const uint32_t k = off + i, rd = rd0 + 2 * k;
+        const double v_prev = (k >= 1) ? __ldg(x + rd - 1) : 0.0;
+        a[h] = __ldg(x + rd + 1) - __ldg(x + rd) - v_prev;
+      }
+    }
+  } else if (kind == SEG_BCAP) {                   // bcap(g,k): sum_s B(s,g,k)
+    const uint32_t q0 = o.EK + (uint32_t)Bv * (K + 1) + off;
+#pragma unroll
+    for (int h = 0; h < kSegPerLane; ++h) {
+      const int i = lane + 32 * h;
+      if (i < cnt) {
+        a[h] = te_sum_sources(o, x, q0 + i);
+        lo[h] = -INFINITY;
+        hi[h] = o.d.blimit;
+      }
+    }
+  } else if (kind == SEG_INIT) {                   // init(s): generic path
+#pragma unroll
+    for (int h = 0; h < kSegPerLane; ++h) {
+      const int i = lane + 32 * h;
+      if (i < cnt) a[h] = te_row(o, (uint32_t)(off + i), x, lo[h], hi[h]);
+    }
+  }
+}
+
+}  // namespace teccl

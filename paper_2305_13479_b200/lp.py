@@ -240,12 +240,31 @@ class DeviceLP:
                                                  C.byref(ms), C.byref(by)))
         return ms.value, by.value
 
+    def apply(self, v: np.ndarray, transpose: bool = False, matrix_free: int = 1) -> dict:
+        """A.v (or A^T.v) on the device with the bounds (and costs) that path
+        sees: matrix_free = 0 stored CSR/CSC, 1 per-entry matrix-free
+        operator, 2 segment walkers (the PDLP kernels' operator)."""
+        nin, nout = (self.num_rows, self.num_vars) if transpose else (self.num_vars, self.num_rows)
+        v = np.ascontiguousarray(v, dtype=np.float64)
+        if v.shape != (nin,):
+            raise ValueError(f"expected a vector of length {nin}")
+        out = {k: np.empty(nout, np.float64) for k in ("y", "lo", "hi")}
+        out["cost"] = np.empty(nout if transpose else 1, np.float64)
+        nat.check(self.ctx.lib.teccl_lp_apply(
+            self.ctx.handle, self.handle, int(bool(transpose)), int(matrix_free),
+            nat.ptr(v, C.c_double), nat.ptr(out["y"], C.c_double), nat.ptr(out["lo"], C.c_double),
+            nat.ptr(out["hi"], C.c_double), nat.ptr(out["cost"], C.c_double)))
+        if not transpose:
+            del out["cost"]
+        return out
+
     def step_bench(self, reps: int = 50) -> dict:
         """Per-launch device time and algorithmic bytes of the fused kernels."""
         out = (C.c_double * 6)()
         nat.check(self.ctx.lib.teccl_pdlp_step_bench(self.ctx.handle, self.handle, int(reps), out))
         return {"ms_col": out[0], "ms_row": out[1], "bytes_col": out[2], "bytes_row": out[3],
-                "dict": bool(out[4]), "slice": int(out[5])}
+                "dict": out[4] >= 1.0, "matrix_free": out[4] == 2.0,
+                "slice": int(out[5])}
 
     def close(self) -> None:
         if self.handle:
