@@ -59,7 +59,9 @@ struct PdlpState {
   long long k_inner, total;
   int have_r0, restart, done, restarts, chunk_len, pad;
   double rel_p, rel_d, gap, pobj, dobj;
+  double lam_tab[128];       // Halpern weights (k+1)/(k+2) of the current chunk's iterations
 };
+constexpr int kLamTab = 128;
 
 // Per-column / per-row problem data as the iteration kernels see it.
 struct Bounds {
@@ -238,6 +240,15 @@ __global__ void sum_slots_kernel(const double* slots, int world, int count, doub
 // always-zero vector slot. Coalesced index streams, warp-uniform trip counts,
 // no shared memory, no barriers; row order unchanged, so the epilogue is
 // thread-per-row with coalesced vector traffic.
+// v[t & mask] with the sign bit of t applied (unit-coefficient entries):
+// one wide multiply-add for the address, one xor for the sign
+__device__ __forceinline__ double sgather(const double* __restrict__ v, uint32_t t) {
+  uint64_t off;
+  asm("mul.wide.u32 %0, %1, 8;" : "=l"(off) : "r"(t & kIdxMask));
+  const double xv = __ldg(reinterpret_cast<const double*>(reinterpret_cast<const char*>(v) + off));
+  return __hiloint2double(__double2hiint(xv) ^ (int)(t & kSignBit), __double2loint(xv));
+}
+
 struct SellView {
   const int64_t* off;
   const int32_t* width;
@@ -264,8 +275,7 @@ __device__ __forceinline__ double sell_dot(const SellView& S, int64_t r,
     for (int u = 0; u < G; ++u) {
       if (q + u < w) {
         if (UNIT) {
-          const double xv = __ldg(v + (t[u] & kIdxMask));
-          acc += (t[u] & kSignBit) ? -xv : xv;
+          acc += sgather(v, t[u]);
         } else {
           acc += __ldg(vp + (q + u) * kSlice) * __ldg(v + t[u]);
         }
@@ -351,8 +361,7 @@ __global__ void __launch_bounds__(kThreads) col_step_kernel(int32_t n, SellView 
   const PdlpState* st = V.st;
   const int done = st->done;  // checked before the first store: the gathers overlap it
   const double tau = st->tau, refl = st->refl;
-  const double kk = (double)(st->k_inner + j_in_chunk);
-  const double lam = (kk + 1.0) / (kk + 2.0);
+  const double lam = st->lam_tab[j_in_chunk];  // chunks are at most kLamTab iterations
   const double s = (j < n) ? sell_dot<UNIT>(S, j, V.y) : 0.0;
   if (done) return;
   double dx = 0.0, dx0 = 0.0;
@@ -400,8 +409,7 @@ __global__ void __launch_bounds__(kThreads) col_pipe_kernel(int32_t n, SellView 
   const PdlpState* st = V.st;
   const int done = st->done;
   const double tau = st->tau, refl = st->refl;
-  const double kk = (double)(st->k_inner + j_in_chunk);
-  const double lam = (kk + 1.0) / (kk + 2.0);
+  const double lam = st->lam_tab[j_in_chunk];  // chunks are at most kLamTab iterations
   if (done) return;
   double dx = 0.0, dx0 = 0.0;
   while (j < n) {
@@ -424,8 +432,7 @@ __global__ void __launch_bounds__(kThreads) col_pipe_kernel(int32_t n, SellView 
     for (int u = 0; u < 4; ++u) {
       if (u < w) {
         if (UNIT) {
-          const double xv = __ldg(V.y + (t[u] & kIdxMask));
-          s += (t[u] & kSignBit) ? -xv : xv;
+          s += sgather(V.y, t[u]);
         } else {
           s += __ldg(S.val + base + (int64_t)u * kSlice) * __ldg(V.y + t[u]);
         }
@@ -434,8 +441,7 @@ __global__ void __launch_bounds__(kThreads) col_pipe_kernel(int32_t n, SellView 
     for (int q = 4; q < w; ++q) {  // columns wider than 4 (rare)
       const uint32_t tq = __ldg(S.idx + base + (int64_t)q * kSlice);
       if (UNIT) {
-        const double xv = __ldg(V.y + (tq & kIdxMask));
-        s += (tq & kSignBit) ? -xv : xv;
+        s += sgather(V.y, tq);
       } else {
         s += __ldg(S.val + base + (int64_t)q * kSlice) * __ldg(V.y + tq);
       }
@@ -485,8 +491,7 @@ __global__ void __launch_bounds__(kThreads) row_step_kernel(int32_t m, SellView 
   const PdlpState* st = V.st;
   const int done = st->done;  // checked before the first store: the gathers overlap it
   const double sigma = st->sigma, refl = st->refl;
-  const double kk = (double)(st->k_inner + j_in_chunk);
-  const double lam = (kk + 1.0) / (kk + 2.0);
+  const double lam = st->lam_tab[j_in_chunk];  // chunks are at most kLamTab iterations
   const double s = (i < m) ? sell_dot<UNIT, 8>(S, i, V.xbar) : 0.0;
   if (done) return;
   double dy = 0.0, dy0 = 0.0;
@@ -530,10 +535,9 @@ __global__ void __launch_bounds__(kThreads) col_te_kernel(TeOp op, Vecs V, int j
   const PdlpState* st = V.st;
   const int done = st->done;  // checked before the first store: the gathers overlap it
   const double tau = st->tau, refl = st->refl;
-  const double kk = (double)(st->k_inner + j_in_chunk);
   if (j < op.n) s = te_col(op, j, V.y, lb, ub, cj);
   if (done) return;
-  const double lam = (kk + 1.0) / (kk + 2.0);
+  const double lam = st->lam_tab[j_in_chunk];  // chunks are at most kLamTab iterations
   double dx = 0.0, dx0 = 0.0;
   if (j < op.n) {
     const double xt = clampd(xj - tau * Dj * (cj - s), lb, ub);
@@ -569,10 +573,9 @@ __global__ void __launch_bounds__(kThreads) row_te_kernel(TeOp op, Vecs V, int j
   const PdlpState* st = V.st;
   const int done = st->done;  // checked before the first store: the gathers overlap it
   const double sigma = st->sigma, refl = st->refl;
-  const double kk = (double)(st->k_inner + j_in_chunk);
   if (i < op.m) s = te_row(op, i, V.xbar, lo, hi);
   if (done) return;
-  const double lam = (kk + 1.0) / (kk + 2.0);
+  const double lam = st->lam_tab[j_in_chunk];  // chunks are at most kLamTab iterations
   double dy = 0.0, dy0 = 0.0;
   if (i < op.m) {
     const double se = sigma * Ei;
@@ -620,11 +623,10 @@ __global__ void __launch_bounds__(kThreads) col_seg_kernel(TeOp op, Vecs V, int 
   const PdlpState* st = V.st;
   const int done = st->done;
   const double tau = st->tau, refl = st->refl;
-  const double kk = (double)(st->k_inner + j_in_chunk);
   double s[kSegPerLane], lb[kSegPerLane], ub[kSegPerLane], cj[kSegPerLane];
   seg_cols(op, tk, lane, V.y, s, lb, ub, cj);
   if (done) return;
-  const double lam = (kk + 1.0) / (kk + 2.0);
+  const double lam = st->lam_tab[j_in_chunk];  // chunks are at most kLamTab iterations
   double dx = 0.0, dx0 = 0.0;
 #pragma unroll
   for (int h = 0; h < kSegPerLane; ++h) {
@@ -673,11 +675,10 @@ __global__ void __launch_bounds__(kThreads) row_seg_kernel(TeOp op, Vecs V, int 
   const PdlpState* st = V.st;
   const int done = st->done;
   const double sigma = st->sigma, refl = st->refl;
-  const double kk = (double)(st->k_inner + j_in_chunk);
   double s[kSegPerLane], lo[kSegPerLane], hi[kSegPerLane];
   seg_rows(op, tk, lane, V.xbar, s, lo, hi);
   if (done) return;
-  const double lam = (kk + 1.0) / (kk + 2.0);
+  const double lam = st->lam_tab[j_in_chunk];  // chunks are at most kLamTab iterations
   double dy = 0.0, dy0 = 0.0;
 #pragma unroll
   for (int h = 0; h < kSegPerLane; ++h) {
@@ -775,9 +776,8 @@ __global__ void __launch_bounds__(kThreads) kkt_col_kernel(int32_t n, SellView S
 // Sum every rank's reduced partials in rank order (identical on all ranks, so
 // all ranks take the same decisions), evaluate termination, decide restarts
 // and update the primal weight. All of PDLP's control flow.
-__global__ void control_kernel(Vecs V) {
+__device__ void control_decide(Vecs V) {
   PdlpState* st = V.st;
-  if (threadIdx.x != 0 || st->done) return;
   double q[kNQ];
   for (int k = 0; k < kNQ; ++k) {
     double a = 0.0;
@@ -829,6 +829,19 @@ __global__ void control_kernel(Vecs V) {
       st->tau = st->eta / st->omega;
       st->sigma = st->eta * st->omega;
     }
+  }
+}
+
+__global__ void control_kernel(Vecs V) {
+  PdlpState* st = V.st;
+  if (st->done) return;
+  if (threadIdx.x == 0) control_decide(V);
+  __syncwarp();
+  // Halpern weights of the next chunk's iterations
+  const long long k0 = st->k_inner;
+  for (int j = threadIdx.x; j < kLamTab; j += 32) {
+    const double kk = (double)(k0 + j);
+    st->lam_tab[j] = (kk + 1.0) / (kk + 2.0);
   }
 }
 
@@ -1493,8 +1506,9 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
   hs.theta = o->omega_theta;
   hs.ki = o->omega_ki;
   hs.kd = o->omega_kd;
-  const int chunk = o->check_every > 0 ? o->check_every : 64;
+  const int chunk = std::min(o->check_every > 0 ? o->check_every : 64, kLamTab);
   hs.chunk_len = chunk;
+  for (int j = 0; j < kLamTab; ++j) hs.lam_tab[j] = (j + 1.0) / (j + 2.0);
   TECCL_CUDA(cudaMemcpyAsync(dst, &hs, sizeof(hs), cudaMemcpyHostToDevice, st));
 
   Vecs V{};
