@@ -43,6 +43,17 @@
 
 namespace teccl {
 
+// build-time knobs of the row half-step (A/B builds: tools/build_variant.sh)
+#ifndef TECCL_ROW_G
+#define TECCL_ROW_G 8      // index loads in flight per row group
+#endif
+#ifndef TECCL_ROW_MINB
+#define TECCL_ROW_MINB 1   // __launch_bounds__ min blocks per SM
+#endif
+#ifndef TECCL_COL_MINB
+#define TECCL_COL_MINB 4   // same, pipelined column kernel (64 registers: measured best)
+#endif
+
 constexpr int kGrid = kSMs * 8;  // blocks of the setup reduction kernels
 constexpr int kNQ = 9;           // partial quantities per check
 constexpr int kSlice = 32;
@@ -389,7 +400,7 @@ __global__ void __launch_bounds__(kThreads) col_step_kernel(int32_t n, SellView 
 // header and index loads of its next column j + stride are already in
 // flight, so each column costs about one memory latency instead of three.
 template <bool UNIT, bool DICT, bool CHECK>
-__global__ void __launch_bounds__(kThreads) col_pipe_kernel(int32_t n, SellView S, Vecs V,
+__global__ void __launch_bounds__(kThreads, TECCL_COL_MINB) col_pipe_kernel(int32_t n, SellView S, Vecs V,
                                                             int j_in_chunk) {
   __shared__ double sh[32];
   const int64_t stride = (int64_t)gridDim.x * kThreads;
@@ -475,7 +486,7 @@ __global__ void __launch_bounds__(kThreads) col_pipe_kernel(int32_t n, SellView 
 
 // Dual half-step over rows (CSR as SELL), fused with A.xbar.
 template <bool UNIT, bool DICT, bool CHECK>
-__global__ void __launch_bounds__(kThreads) row_step_kernel(int32_t m, SellView S, Vecs V,
+__global__ void __launch_bounds__(kThreads, TECCL_ROW_MINB) row_step_kernel(int32_t m, SellView S, Vecs V,
                                                             int j_in_chunk) {
   __shared__ double sh[32];
   const int64_t i = (int64_t)blockIdx.x * kTile + threadIdx.x;
@@ -492,7 +503,7 @@ __global__ void __launch_bounds__(kThreads) row_step_kernel(int32_t m, SellView 
   const int done = st->done;  // checked before the first store: the gathers overlap it
   const double sigma = st->sigma, refl = st->refl;
   const double lam = st->lam_tab[j_in_chunk];  // chunks are at most kLamTab iterations
-  const double s = (i < m) ? sell_dot<UNIT, 8>(S, i, V.xbar) : 0.0;
+  const double s = (i < m) ? sell_dot<UNIT, TECCL_ROW_G>(S, i, V.xbar) : 0.0;
   if (done) return;
   double dy = 0.0, dy0 = 0.0;
   if (i < m) {

@@ -15,6 +15,9 @@ lp = build_from_plan(make_plan(t, d, cfg))
 variants = [dict(matrix_free=mf, pdl=pdl, col_pipeline=cp)
             for mf, pdl, cp in itertools.product((3, 2, 0), (1, 0), (1,))]
 variants.append(dict(matrix_free=0, pdl=1, col_pipeline=0))
+if os.environ.get("VARIANTS"):  # e.g. '[{"matrix_free": 0, "pdl": 1, "col_pipeline": 1}]'
+    import json
+    variants = json.loads(os.environ["VARIANTS"])
 for v in variants:
     opts = SolverOptions(eps_rel=1e-4, pdlp=v)
     best = None
@@ -23,6 +26,6 @@ for v in variants:
         if best is None or s.meta["device_seconds"] < best.meta["device_seconds"]:
             best = s
     sb = lp.step_bench(100) if v["pdl"] == 1 else None
-    print(v, best.meta["iters"], round(best.meta["device_seconds"], 4),
+    print(os.path.basename(os.environ.get("TECCL_B200_LIB", "default")), v, best.meta["iters"], round(best.meta["device_seconds"], 4),
           round(1e6 * best.meta["device_seconds"] / best.meta["iters"], 2), "us/it",
           round(best.objective, 6), flush=True)
