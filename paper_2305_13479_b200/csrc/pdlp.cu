@@ -269,9 +269,9 @@ struct SellView {
 };
 
 template <bool UNIT, int G = 4>
-__device__ __forceinline__ double sell_dot(const SellView& S, int64_t r,
+__device__ __forceinline__ double sell_dot(const SellView& S, uint32_t r,
                                            const double* __restrict__ v) {
-  const int64_t s = r >> 5;
+  const uint32_t s = r >> 5;
   const int w = __ldg(S.width + s);
   const uint32_t* ip = S.idx + __ldg(S.off + s) + (r & 31);
   const double* vp = UNIT ? nullptr : S.val + (ip - S.idx);
@@ -403,13 +403,15 @@ template <bool UNIT, bool DICT, bool CHECK>
 __global__ void __launch_bounds__(kThreads, TECCL_COL_MINB) col_pipe_kernel(int32_t n, SellView S, Vecs V,
                                                             int j_in_chunk) {
   __shared__ double sh[32];
-  const int64_t stride = (int64_t)gridDim.x * kThreads;
-  int64_t j = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  // 32-bit column ids (n < 2^31); 64-bit SELL offsets
+  const uint32_t un = (uint32_t)n;
+  const uint32_t stride = gridDim.x * kThreads;
+  uint32_t j = blockIdx.x * kThreads + threadIdx.x;
   // stage 1 of the first column: slice header and up to 4 indices
   int w = 0;
   int64_t base = 0;
   uint32_t t[4] = {0u, 0u, 0u, 0u};
-  if (j < n) {
+  if (j < un) {
     w = __ldg(S.width + (j >> 5));
     base = __ldg(S.off + (j >> 5)) + (j & 31);
 #pragma unroll
@@ -423,12 +425,12 @@ __global__ void __launch_bounds__(kThreads, TECCL_COL_MINB) col_pipe_kernel(int3
   const double lam = st->lam_tab[j_in_chunk];  // chunks are at most kLamTab iterations
   if (done) return;
   double dx = 0.0, dx0 = 0.0;
-  while (j < n) {
-    const int64_t jn = j + stride;
+  while (j < un) {
+    const uint32_t jn = j + stride;
     // next column's slice header: independent of this column's work
     int wn = 0;
     int64_t basen = 0;
-    if (jn < n) {
+    if (jn < un) {
       wn = __ldg(S.width + (jn >> 5));
       basen = __ldg(S.off + (jn >> 5)) + (jn & 31);
     }
@@ -489,9 +491,9 @@ template <bool UNIT, bool DICT, bool CHECK>
 __global__ void __launch_bounds__(kThreads, TECCL_ROW_MINB) row_step_kernel(int32_t m, SellView S, Vecs V,
                                                             int j_in_chunk) {
   __shared__ double sh[32];
-  const int64_t i = (int64_t)blockIdx.x * kTile + threadIdx.x;
+  const uint32_t i = blockIdx.x * kTile + threadIdx.x;  // m < 2^31
   double yi = 0.0, y0 = 0.0, Ei = 0.0, lo = 0.0, hi = 0.0;
-  if (i < m) {
+  if (i < (uint32_t)m) {
     yi = V.y[i];
     y0 = (double)V.y0[i];
     Ei = (double)V.E[i];
@@ -503,10 +505,10 @@ __global__ void __launch_bounds__(kThreads, TECCL_ROW_MINB) row_step_kernel(int3
   const int done = st->done;  // checked before the first store: the gathers overlap it
   const double sigma = st->sigma, refl = st->refl;
   const double lam = st->lam_tab[j_in_chunk];  // chunks are at most kLamTab iterations
-  const double s = (i < m) ? sell_dot<UNIT, TECCL_ROW_G>(S, i, V.xbar) : 0.0;
+  const double s = (i < (uint32_t)m) ? sell_dot<UNIT, TECCL_ROW_G>(S, i, V.xbar) : 0.0;
   if (done) return;
   double dy = 0.0, dy0 = 0.0;
-  if (i < m) {
+  if (i < (uint32_t)m) {
     const double se = sigma * Ei;
     const double yt = yi - se * (s - clampd(s - yi / se, lo, hi));
     V.y[i] = lam * ((1.0 + refl) * yt - refl * yi) + (1.0 - lam) * y0;
