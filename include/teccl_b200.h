@@ -151,6 +151,9 @@ typedef struct {
                                  per-entry), 2 per-entry, 3 segment kernels (0) */
   int32_t pdl;                /* 1: programmatic dependent launch between the iteration
                                  kernels (prologue of one overlaps the tail of the last) (1) */
+  int32_t fused_halo;         /* row-partitioned solves: the half-step kernels store their
+                                 boundary outputs into the neighbours' windows over peer
+                                 memory and signal, instead of separate halo kernels (1) */
 } teccl_pdlp_opts;
 
 typedef struct {

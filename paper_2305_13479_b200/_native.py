@@ -55,6 +55,7 @@ class PdlpOpts(C.Structure):
         ("omega_theta", C.c_double), ("omega_scale", C.c_double),
         ("omega_ki", C.c_double), ("omega_kd", C.c_double), ("col_pipeline", C.c_int32),
         ("matrix_free", C.c_int32), ("pdl", C.c_int32),
+        ("fused_halo", C.c_int32),
     ]
 
 

@@ -74,38 +74,6 @@ struct PdlpState {
 };
 constexpr int kLamTab = 128;
 
-// Per-column / per-row problem data as the iteration kernels see it.
-struct Bounds {
-  const uint16_t* code;  // class code, or nullptr: read the explicit arrays
-  const double* dict;    // classes: (lb, ub, c) for columns, (lo, hi) for rows
-  const double* a;       // explicit lb (cols) / lo (rows)
-  const double* b;       // explicit ub / hi
-  const double* c;       // explicit cost (cols only)
-};
-
-struct Vecs {
-  const float* D;        // column preconditioner C^2
-  const float* E;        // row preconditioner R^2
-  Bounds col, row;
-  double *x, *xt, *xbar; // xbar has an always-zero slot [n] (SELL padding)
-  float* x0;
-  double *y, *yt;        // y, yt have an always-zero slot [m]
-  float* y0;
-  // exact unscaled data for the KKT evaluation
-  const double *c_u, *lb_u, *ub_u, *lo_u, *hi_u;
-  double* part;          // [kNQ * pstride]
-  int64_t pstride;
-  int nb_row, nb_col;
-  PdlpState* st;
-  double* slots;         // [world][kSlots]: every rank's reduced partials
-  int world, rank;
-  int col_pipe;          // column half-step: pipelined resident grid (1) or one thread per column (0)
-  int pdl;               // iteration kernels launched with programmatic dependent launch
-  int seg;               // matrix-free: segment-walking kernels (1) or one thread per entry (0)
-};
-
-__device__ __forceinline__ double block_sum(double v, double* sh);
-
 constexpr int kSlots = 16;  // doubles per rank in the slot table
 constexpr int kMaxPeers = 8;
 
@@ -145,11 +113,106 @@ __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned l
   asm volatile("st.release.sys.global.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
 }
 
+// Fused peer exchange of a half-step kernel (row-partitioned solves): its
+// owned outputs that fall inside a neighbour's gather window are stored
+// straight into that window over NVLink (the value array, and the check
+// array on check iterations), and the last block to finish publishes the
+// next sequence number; `wait` is the neighbours' previous signal, awaited
+// before the kernel gathers. n = 0 on one device.
+struct Push {
+  double* dv[2];          // neighbour window at owned-local index lo (xbar or y)
+  double* dc[2];          // same for the check array (xt or yt)
+  int64_t lo[2], hi[2];   // owned-local index range each neighbour needs
+  int n;
+  Signal sig;
+};
+
+// Per-column / per-row problem data as the iteration kernels see it.
+struct Bounds {
+  const uint16_t* code;  // class code, or nullptr: read the explicit arrays
+  const double* dict;    // classes: (lb, ub, c) for columns, (lo, hi) for rows
+  const double* a;       // explicit lb (cols) / lo (rows)
+  const double* b;       // explicit ub / hi
+  const double* c;       // explicit cost (cols only)
+};
+
+struct Vecs {
+  const float* D;        // column preconditioner C^2
+  const float* E;        // row preconditioner R^2
+  Bounds col, row;
+  double *x, *xt, *xbar; // xbar has an always-zero slot [n] (SELL padding)
+  float* x0;
+  double *y, *yt;        // y, yt have an always-zero slot [m]
+  float* y0;
+  // exact unscaled data for the KKT evaluation
+  const double *c_u, *lb_u, *ub_u, *lo_u, *hi_u;
+  double* part;          // [kNQ * pstride]
+  int64_t pstride;
+  int nb_row, nb_col;
+  PdlpState* st;
+  double* slots;         // [world][kSlots]: every rank's reduced partials
+  int world, rank;
+  int col_pipe;          // column half-step: pipelined resident grid (1) or one thread per column (0)
+  int pdl;               // iteration kernels launched with programmatic dependent launch
+  int seg;               // matrix-free: segment-walking kernels (1) or one thread per entry (0)
+  Push push;             // fused halo out (see Push)
+  Wait wait;             // fused halo in: neighbours' signal awaited before gathering
+};
+
+__device__ __forceinline__ double block_sum(double v, double* sh);
+
 __device__ __forceinline__ void signal_peers(const Signal& S) {
   const unsigned long long s = *S.seq + 1;
   *S.seq = s;
   __threadfence_system();
   for (int q = 0; q < S.npeer; ++q) st_release_sys(S.peer_flag[q], s);
+}
+
+// Fused halo, consumer side: thread 0 of every block waits (acquire, system
+// scope) for the neighbours' current sequence number; false on timeout
+// (the solve then stops with done = 4 on this rank).
+__device__ __forceinline__ bool block_wait_peers(const Wait& W, PdlpState* st) {
+  __shared__ int ok;
+  if (threadIdx.x == 0) {
+    ok = 1;
+    const unsigned long long want = *W.seq;
+    const long long t0 = clock64();
+    for (int q = 0; q < W.npeer && ok; ++q)
+      while (ld_acquire_sys(W.flags + W.peer[q]) < want) {
+        __nanosleep(64);
+        if (clock64() - t0 > 40000000000LL) { st->done = 4; ok = 0; break; }
+      }
+  }
+  __syncthreads();
+  return ok != 0;
+}
+
+// Fused halo, producer side: store entry j's outputs into every neighbour
+// window that holds it.
+template <bool CHECK>
+__device__ __forceinline__ bool push_entry(const Push& P, int64_t j, double v, double c) {
+  bool wrote = false;
+  for (int r = 0; r < P.n; ++r)
+    if (j >= P.lo[r] && j < P.hi[r]) {
+      P.dv[r][j - P.lo[r]] = v;
+      if (CHECK) P.dc[r][j - P.lo[r]] = c;
+      wrote = true;
+    }
+  return wrote;
+}
+
+// ... and at the end of the kernel: the last block publishes the signal.
+__device__ __forceinline__ void push_signal(const Push& P, bool wrote) {
+  if (P.n == 0) return;
+  if (wrote) __threadfence_system();  // this thread's peer stores before the block's arrival
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int prev = atomicAdd(P.sig.arrive, 1u);
+    if (prev == gridDim.x - 1) {
+      *P.sig.arrive = 0u;
+      signal_peers(P.sig);
+    }
+  }
 }
 
 // Copy every (src -> peer dst) range, then the last block to finish signals.
@@ -373,12 +436,16 @@ __global__ void __launch_bounds__(kThreads) col_step_kernel(int32_t n, SellView 
   const int done = st->done;  // checked before the first store: the gathers overlap it
   const double tau = st->tau, refl = st->refl;
   const double lam = st->lam_tab[j_in_chunk];  // chunks are at most kLamTab iterations
+  if (V.wait.npeer && (done || !block_wait_peers(V.wait, V.st))) return;
   const double s = (j < n) ? sell_dot<UNIT>(S, j, V.y) : 0.0;
   if (done) return;
+  bool wrote = false;
   double dx = 0.0, dx0 = 0.0;
   if (j < n) {
     const double xt = clampd(xj - tau * Dj * (cj - s), lb, ub);
-    V.xbar[j] = 2.0 * xt - xj;
+    const double xb = 2.0 * xt - xj;
+    V.xbar[j] = xb;
+    wrote = push_entry<CHECK>(V.push, j, xb, xt);
     V.x[j] = lam * ((1.0 + refl) * xt - refl * xj) + (1.0 - lam) * x0;
     if (CHECK) {
       V.xt[j] = xt;
@@ -393,6 +460,7 @@ __global__ void __launch_bounds__(kThreads) col_step_kernel(int32_t n, SellView 
     a = block_sum(dx0, sh);
     if (threadIdx.x == 0) V.part[Q_DX0 * V.pstride + blockIdx.x] = a;
   }
+  push_signal(V.push, wrote);
 }
 
 // Software-pipelined variant of col_step: a resident grid walks the columns
@@ -424,7 +492,9 @@ __global__ void __launch_bounds__(kThreads, TECCL_COL_MINB) col_pipe_kernel(int3
   const double tau = st->tau, refl = st->refl;
   const double lam = st->lam_tab[j_in_chunk];  // chunks are at most kLamTab iterations
   if (done) return;
+  if (V.wait.npeer && !block_wait_peers(V.wait, V.st)) return;
   double dx = 0.0, dx0 = 0.0;
+  bool wrote = false;
   while (j < un) {
     const uint32_t jn = j + stride;
     // next column's slice header: independent of this column's work
@@ -464,7 +534,9 @@ __global__ void __launch_bounds__(kThreads, TECCL_COL_MINB) col_pipe_kernel(int3
 #pragma unroll
     for (int u = 0; u < 4; ++u) tn[u] = (u < wn) ? __ldg(S.idx + basen + (int64_t)u * kSlice) : 0u;
     const double xt = clampd(xj - tau * Dj * (cj - s), lb, ub);
-    V.xbar[j] = 2.0 * xt - xj;
+    const double xb = 2.0 * xt - xj;
+    V.xbar[j] = xb;
+    wrote |= push_entry<CHECK>(V.push, j, xb, xt);
     V.x[j] = lam * ((1.0 + refl) * xt - refl * xj) + (1.0 - lam) * x0;
     if (CHECK) {
       V.xt[j] = xt;
@@ -484,6 +556,7 @@ __global__ void __launch_bounds__(kThreads, TECCL_COL_MINB) col_pipe_kernel(int3
     a = block_sum(dx0, sh);
     if (threadIdx.x == 0) V.part[Q_DX0 * V.pstride + blockIdx.x] = a;
   }
+  push_signal(V.push, wrote);
 }
 
 // Dual half-step over rows (CSR as SELL), fused with A.xbar.
@@ -505,13 +578,17 @@ __global__ void __launch_bounds__(kThreads, TECCL_ROW_MINB) row_step_kernel(int3
   const int done = st->done;  // checked before the first store: the gathers overlap it
   const double sigma = st->sigma, refl = st->refl;
   const double lam = st->lam_tab[j_in_chunk];  // chunks are at most kLamTab iterations
+  if (V.wait.npeer && (done || !block_wait_peers(V.wait, V.st))) return;
   const double s = (i < (uint32_t)m) ? sell_dot<UNIT, TECCL_ROW_G>(S, i, V.xbar) : 0.0;
   if (done) return;
+  bool wrote = false;
   double dy = 0.0, dy0 = 0.0;
   if (i < (uint32_t)m) {
     const double se = sigma * Ei;
     const double yt = yi - se * (s - clampd(s - yi / se, lo, hi));
-    V.y[i] = lam * ((1.0 + refl) * yt - refl * yi) + (1.0 - lam) * y0;
+    const double yn = lam * ((1.0 + refl) * yt - refl * yi) + (1.0 - lam) * y0;
+    V.y[i] = yn;
+    wrote = push_entry<CHECK>(V.push, i, yn, yt);
     if (CHECK) {
       V.yt[i] = yt;
       const double w = 1.0 / Ei;
@@ -525,6 +602,7 @@ __global__ void __launch_bounds__(kThreads, TECCL_ROW_MINB) row_step_kernel(int3
     a = block_sum(dy0, sh);
     if (threadIdx.x == 0) V.part[Q_DY0 * V.pstride + blockIdx.x] = a;
   }
+  push_signal(V.push, wrote);
 }
 
 // ---------------------------------------------------------------------------
@@ -1105,6 +1183,25 @@ struct DistState {
       }
     return H;
   }
+  // fused-halo plan of a half-step kernel: value array idv, check array idc
+  Push push_plan(int idv, int idc) const {
+    Push P{};
+    for (int q : {rank - 1, rank + 1}) {
+      if (q < 0 || q >= world || P.n >= 2) continue;
+      int64_t o0, o1, w0, w1, qo0, qo1, qw0, qw1;
+      range(rank, idv, o0, o1, w0, w1);
+      range(q, idv, qo0, qo1, qw0, qw1);
+      const int64_t a = std::max(o0, qw0), b = std::min(o1, qw1);
+      if (b <= a) continue;
+      P.lo[P.n] = a - o0;
+      P.hi[P.n] = b - o0;
+      P.dv[P.n] = (double*)(peer_base[q] + peer_meta[q][M_OFF0 + idv]) + (a - qw0);
+      P.dc[P.n] = (double*)(peer_base[q] + peer_meta[q][M_OFF0 + idc]) + (a - qw0);
+      ++P.n;
+    }
+    P.sig = sig_nbr;
+    return P;
+  }
   int64_t halo_max(std::initializer_list<int> ids) const {
     Halo H = halo_plan(ids);
     int64_t mx = 1;
@@ -1261,6 +1358,11 @@ struct Exchange {
     wait_kernel<<<1, 32, 0, s>>>(ds->wait_nbr, st);
     nl += 2;
   }
+  void wait_nbr(cudaStream_t s) {
+    if (!active()) return;
+    wait_kernel<<<1, 32, 0, s>>>(ds->wait_nbr, st);
+    nl += 1;
+  }
   void wait_all(cudaStream_t s) {
     if (!active()) return;
     wait_kernel<<<1, 32, 0, s>>>(ds->wait_all, st);
@@ -1276,13 +1378,22 @@ void enqueue_chunk(int chunk, cudaStream_t st, const teccl_lp* lp, const TeOp* t
     const bool check = (j == chunk - 1);
     if (check) launch_col<UNIT, DICT, true>(st, lp, te, Vc, j);
     else launch_col<UNIT, DICT, false>(st, lp, te, Vc, j);
-    if (check) X.halo(st, {A_XBAR, A_XT});
-    else X.halo(st, {A_XBAR});
+    if (!Vc.push.n) {  // fused kernels push their own halos
+      if (check) X.halo(st, {A_XBAR, A_XT});
+      else X.halo(st, {A_XBAR});
+    } else if (!Vr.wait.npeer) {
+      X.wait_nbr(st);  // fused_halo = 2: the wait is a separate one-thread kernel
+    }
     if (check) launch_row<UNIT, DICT, true>(st, lp, te, Vr, j);
     else launch_row<UNIT, DICT, false>(st, lp, te, Vr, j);
-    if (check) X.halo(st, {A_Y, A_YT});
-    else X.halo(st, {A_Y});
+    if (!Vr.push.n) {
+      if (check) X.halo(st, {A_Y, A_YT});
+      else X.halo(st, {A_Y});
+    } else if (!Vc.wait.npeer) {
+      X.wait_nbr(st);
+    }
   }
+  if (Vr.push.n) X.wait_nbr(st);  // yt ghosts for kkt_col
   if (te) {
     kkt_row_kernel<UNIT, true><<<Vr.nb_row, kThreads, 0, st>>>(lp->m, SellView{}, *te, Vr);
     kkt_col_kernel<UNIT, true><<<Vc.nb_col, kThreads, 0, st>>>(lp->n, SellView{}, *te, Vc);
@@ -1553,6 +1664,14 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
   Vc.xt = xt; Vc.xbar = xbar; Vc.y = y_w; Vc.yt = yt_w;
   Vr.y = y; Vr.yt = yt; Vr.xbar = xbar_w; Vr.xt = xt_w;
   Vi.xt = xt; Vi.xbar = xbar; Vi.y = y; Vi.yt = yt;
+  if (X.active() && o->fused_halo) {  // halos stored by the half-step kernels themselves
+    Vc.push = ds->push_plan(A_XBAR, A_XT);
+    Vr.push = ds->push_plan(A_Y, A_YT);
+    if (o->fused_halo == 1) {  // 2: waits stay separate one-thread kernels
+      Vc.wait = ds->wait_nbr;
+      Vr.wait = ds->wait_nbr;
+    }
+  }
   init_iterates_kernel<<<gr, kThreads, 0, st>>>(n, m, Vi, o->warm_start, x_dev, y_dev);
   nl += 1;
   if (o->warm_start) X.halo(st, {A_Y, A_YT});
@@ -1599,7 +1718,7 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
   }
 
   // --- chunk graph (captured once per LP and chunk length)
-  const int graph_key = chunk * 16 + (o->col_pipeline ? 1 : 0) + (te ? 2 : 0) + (o->pdl ? 4 : 0) + (seg ? 8 : 0);
+  const int graph_key = chunk * 64 + (o->col_pipeline ? 1 : 0) + (te ? 2 : 0) + (o->pdl ? 4 : 0) + (seg ? 8 : 0) + 16 * o->fused_halo;
   if (o->use_graphs && W.gexec && W.graph_chunk != graph_key) {
     cudaGraphExecDestroy(W.gexec);
     W.gexec = nullptr;
@@ -1620,7 +1739,7 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
     W.graph_chunk = graph_key;
   }
   cudaGraphExec_t gexec = o->use_graphs ? W.gexec : nullptr;
-  per_chunk = 2LL * chunk + 6 + (X.active() ? 4LL * chunk + 1 : 0);
+  per_chunk = 2LL * chunk + 6 + (X.active() ? (Vc.push.n || Vr.push.n ? (Vc.wait.npeer ? 2LL : 2LL * chunk + 2) : 4LL * chunk + 1) : 0);
   mark("graph");
 
   // --- iterate: chunks queued `lookahead` deep; the device stops itself
@@ -1743,6 +1862,7 @@ extern "C" void teccl_pdlp_default_opts(teccl_pdlp_opts* o) {
   o->col_pipeline = 1;
   o->matrix_free = 0;  // measured: the SELL kernels are faster on configs[1] (profiles/r01_h)
   o->pdl = 1;
+  o->fused_halo = 1;
 }
 
 extern "C" int teccl_pdlp_solve_dev(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* opts,

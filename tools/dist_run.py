@@ -34,8 +34,9 @@ t = ndv2(chassis)
 d = generate_demand("allgather", t, chunks, 25000)
 cfg = EpochConfig(epoch_duration(t, d.chunk_size, "fastest", 1), K, "fastest", 1, d.chunk_size)
 t0 = time.perf_counter()
+pdlp = json.loads(os.environ.get("PDLP_OPTS", "{}"))  # e.g. '{"fused_halo": 0}'
 out = solve_partitioned(t, d, cfg, eps_rel=eps, device=local, gather=bool(compare),
-                        max_iters=max_iters)
+                        max_iters=max_iters, pdlp=pdlp)
 wall = time.perf_counter() - t0
 secs = torch.tensor([out["device_seconds"]], dtype=torch.float64, device=f"cuda:{local}")
 dist.all_reduce(secs, op=dist.ReduceOp.MAX)
@@ -43,7 +44,8 @@ line = {"workload": f"ALLGATHER {chassis}-chassis NDv2, {chunks} chunk(s), K={K}
         "n_gpus": world, "eps_rel": eps, "status": out["status"], "iters": out["iters"],
         "objective": out["objective"], "device_seconds_max": float(secs), "wall_s": wall,
         "per_rank_epochs": [out["info"]["k0"], out["info"]["k1"]], "cols": out["info"]["total_cols"],
-        "rows": out["info"]["total_rows"], "kernel_launches": out["kernel_launches"]}
+        "rows": out["info"]["total_rows"], "kernel_launches": out["kernel_launches"],
+        "pdlp": pdlp}
 if compare and rank == 0:
     plan = out["plan"]
     x = out["x"]
