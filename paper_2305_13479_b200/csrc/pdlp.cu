@@ -48,7 +48,7 @@ namespace teccl {
 #define TECCL_ROW_G 8      // index loads in flight per row group
 #endif
 #ifndef TECCL_ROW_MINB
-#define TECCL_ROW_MINB 1   // __launch_bounds__ min blocks per SM
+#define TECCL_ROW_MINB 5   // __launch_bounds__ min blocks per SM (48 registers)
 #endif
 #ifndef TECCL_COL_MINB
 #define TECCL_COL_MINB 4   // same, pipelined column kernel (64 registers: measured best)
@@ -417,7 +417,7 @@ __device__ __forceinline__ void row_data(const Bounds& B, int64_t i, double& lo,
 
 // ---------------------------------------------------------------------------
 // Primal half-step over columns (CSC as SELL), fused with A^T.y.
-template <bool UNIT, bool DICT, bool CHECK>
+template <bool UNIT, bool DICT, bool CHECK, bool PEER>
 __global__ void __launch_bounds__(kThreads) col_step_kernel(int32_t n, SellView S, Vecs V,
                                                             int j_in_chunk) {
   __shared__ double sh[32];
@@ -436,7 +436,7 @@ __global__ void __launch_bounds__(kThreads) col_step_kernel(int32_t n, SellView 
   const int done = st->done;  // checked before the first store: the gathers overlap it
   const double tau = st->tau, refl = st->refl;
   const double lam = st->lam_tab[j_in_chunk];  // chunks are at most kLamTab iterations
-  if (V.wait.npeer && (done || !block_wait_peers(V.wait, V.st))) return;
+  if (PEER && V.wait.npeer && (done || !block_wait_peers(V.wait, V.st))) return;
   const double s = (j < n) ? sell_dot<UNIT>(S, j, V.y) : 0.0;
   if (done) return;
   bool wrote = false;
@@ -445,7 +445,7 @@ __global__ void __launch_bounds__(kThreads) col_step_kernel(int32_t n, SellView 
     const double xt = clampd(xj - tau * Dj * (cj - s), lb, ub);
     const double xb = 2.0 * xt - xj;
     V.xbar[j] = xb;
-    wrote = push_entry<CHECK>(V.push, j, xb, xt);
+    wrote = PEER && push_entry<CHECK>(V.push, j, xb, xt);
     V.x[j] = lam * ((1.0 + refl) * xt - refl * xj) + (1.0 - lam) * x0;
     if (CHECK) {
       V.xt[j] = xt;
@@ -460,14 +460,14 @@ __global__ void __launch_bounds__(kThreads) col_step_kernel(int32_t n, SellView 
     a = block_sum(dx0, sh);
     if (threadIdx.x == 0) V.part[Q_DX0 * V.pstride + blockIdx.x] = a;
   }
-  push_signal(V.push, wrote);
+  if (PEER) push_signal(V.push, wrote);
 }
 
 // Software-pipelined variant of col_step: a resident grid walks the columns
 // with a grid stride; while a thread gathers and updates column j, the slice
 // header and index loads of its next column j + stride are already in
 // flight, so each column costs about one memory latency instead of three.
-template <bool UNIT, bool DICT, bool CHECK>
+template <bool UNIT, bool DICT, bool CHECK, bool PEER>
 __global__ void __launch_bounds__(kThreads, TECCL_COL_MINB) col_pipe_kernel(int32_t n, SellView S, Vecs V,
                                                             int j_in_chunk) {
   __shared__ double sh[32];
@@ -492,7 +492,7 @@ __global__ void __launch_bounds__(kThreads, TECCL_COL_MINB) col_pipe_kernel(int3
   const double tau = st->tau, refl = st->refl;
   const double lam = st->lam_tab[j_in_chunk];  // chunks are at most kLamTab iterations
   if (done) return;
-  if (V.wait.npeer && !block_wait_peers(V.wait, V.st)) return;
+  if (PEER && V.wait.npeer && !block_wait_peers(V.wait, V.st)) return;
   double dx = 0.0, dx0 = 0.0;
   bool wrote = false;
   while (j < un) {
@@ -536,7 +536,7 @@ __global__ void __launch_bounds__(kThreads, TECCL_COL_MINB) col_pipe_kernel(int3
     const double xt = clampd(xj - tau * Dj * (cj - s), lb, ub);
     const double xb = 2.0 * xt - xj;
     V.xbar[j] = xb;
-    wrote |= push_entry<CHECK>(V.push, j, xb, xt);
+    wrote |= PEER && push_entry<CHECK>(V.push, j, xb, xt);
     V.x[j] = lam * ((1.0 + refl) * xt - refl * xj) + (1.0 - lam) * x0;
     if (CHECK) {
       V.xt[j] = xt;
@@ -556,11 +556,11 @@ __global__ void __launch_bounds__(kThreads, TECCL_COL_MINB) col_pipe_kernel(int3
     a = block_sum(dx0, sh);
     if (threadIdx.x == 0) V.part[Q_DX0 * V.pstride + blockIdx.x] = a;
   }
-  push_signal(V.push, wrote);
+  if (PEER) push_signal(V.push, wrote);
 }
 
 // Dual half-step over rows (CSR as SELL), fused with A.xbar.
-template <bool UNIT, bool DICT, bool CHECK>
+template <bool UNIT, bool DICT, bool CHECK, bool PEER>
 __global__ void __launch_bounds__(kThreads, TECCL_ROW_MINB) row_step_kernel(int32_t m, SellView S, Vecs V,
                                                             int j_in_chunk) {
   __shared__ double sh[32];
@@ -578,7 +578,7 @@ __global__ void __launch_bounds__(kThreads, TECCL_ROW_MINB) row_step_kernel(int3
   const int done = st->done;  // checked before the first store: the gathers overlap it
   const double sigma = st->sigma, refl = st->refl;
   const double lam = st->lam_tab[j_in_chunk];  // chunks are at most kLamTab iterations
-  if (V.wait.npeer && (done || !block_wait_peers(V.wait, V.st))) return;
+  if (PEER && V.wait.npeer && (done || !block_wait_peers(V.wait, V.st))) return;
   const double s = (i < (uint32_t)m) ? sell_dot<UNIT, TECCL_ROW_G>(S, i, V.xbar) : 0.0;
   if (done) return;
   bool wrote = false;
@@ -588,7 +588,7 @@ __global__ void __launch_bounds__(kThreads, TECCL_ROW_MINB) row_step_kernel(int3
     const double yt = yi - se * (s - clampd(s - yi / se, lo, hi));
     const double yn = lam * ((1.0 + refl) * yt - refl * yi) + (1.0 - lam) * y0;
     V.y[i] = yn;
-    wrote = push_entry<CHECK>(V.push, i, yn, yt);
+    wrote = PEER && push_entry<CHECK>(V.push, i, yn, yt);
     if (CHECK) {
       V.yt[i] = yt;
       const double w = 1.0 / Ei;
@@ -602,7 +602,7 @@ __global__ void __launch_bounds__(kThreads, TECCL_ROW_MINB) row_step_kernel(int3
     a = block_sum(dy0, sh);
     if (threadIdx.x == 0) V.part[Q_DY0 * V.pstride + blockIdx.x] = a;
   }
-  push_signal(V.push, wrote);
+  if (PEER) push_signal(V.push, wrote);
 }
 
 // ---------------------------------------------------------------------------
@@ -1287,7 +1287,7 @@ int pipe_blocks() {
   static int blocks = 0;
   if (!blocks) {
     int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, col_pipe_kernel<true, true, false>, kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, col_pipe_kernel<true, true, false, false>, kThreads, 0);
     blocks = kSMs * (occ > 0 ? occ : 4);
   }
   return blocks;
@@ -1314,6 +1314,16 @@ void launch_iter(bool pdl, void (*k)(KArgs...), int grid, cudaStream_t st, Args.
   cudaLaunchKernelEx(&cfg, k, args...);
 }
 
+template <bool UNIT, bool DICT, bool CHECK, bool PEER>
+void launch_col_t(cudaStream_t st, const teccl_lp* lp, const Vecs& V, int j) {
+  const bool pdl = V.pdl != 0;
+  if (V.col_pipe) {
+    const int blocks = std::min<int>(pipe_blocks(), V.nb_col);
+    launch_iter(pdl, col_pipe_kernel<UNIT, DICT, CHECK, PEER>, blocks, st, (int32_t)lp->n, col_view(lp), V, j);
+  } else {
+    launch_iter(pdl, col_step_kernel<UNIT, DICT, CHECK, PEER>, V.nb_col, st, (int32_t)lp->n, col_view(lp), V, j);
+  }
+}
 template <bool UNIT, bool DICT, bool CHECK>
 void launch_col(cudaStream_t st, const teccl_lp* lp, const TeOp* te, const Vecs& V, int j) {
   const bool pdl = V.pdl != 0;
@@ -1321,11 +1331,10 @@ void launch_col(cudaStream_t st, const teccl_lp* lp, const TeOp* te, const Vecs&
     launch_iter(pdl, col_seg_kernel<CHECK>, (te->n_ctask + 7) / 8, st, *te, V, j);
   } else if (te) {
     launch_iter(pdl, col_te_kernel<CHECK>, (int)((te->n + kTile - 1) / kTile), st, *te, V, j);
-  } else if (V.col_pipe) {
-    const int blocks = std::min<int>(pipe_blocks(), V.nb_col);
-    launch_iter(pdl, col_pipe_kernel<UNIT, DICT, CHECK>, blocks, st, (int32_t)lp->n, col_view(lp), V, j);
+  } else if (V.push.n || V.wait.npeer) {  // fused peer exchange compiled in only where used
+    launch_col_t<UNIT, DICT, CHECK, true>(st, lp, V, j);
   } else {
-    launch_iter(pdl, col_step_kernel<UNIT, DICT, CHECK>, V.nb_col, st, (int32_t)lp->n, col_view(lp), V, j);
+    launch_col_t<UNIT, DICT, CHECK, false>(st, lp, V, j);
   }
 }
 template <bool UNIT, bool DICT, bool CHECK>
@@ -1333,7 +1342,10 @@ void launch_row(cudaStream_t st, const teccl_lp* lp, const TeOp* te, const Vecs&
   const bool pdl = V.pdl != 0;
   if (te && V.seg) launch_iter(pdl, row_seg_kernel<CHECK>, (te->n_rtask + 7) / 8, st, *te, V, j);
   else if (te) launch_iter(pdl, row_te_kernel<CHECK>, (int)((te->m + kTile - 1) / kTile), st, *te, V, j);
-  else launch_iter(pdl, row_step_kernel<UNIT, DICT, CHECK>, V.nb_row, st, (int32_t)lp->m, row_view(lp), V, j);
+  else if (V.push.n || V.wait.npeer)
+    launch_iter(pdl, row_step_kernel<UNIT, DICT, CHECK, true>, V.nb_row, st, (int32_t)lp->m, row_view(lp), V, j);
+  else
+    launch_iter(pdl, row_step_kernel<UNIT, DICT, CHECK, false>, V.nb_row, st, (int32_t)lp->m, row_view(lp), V, j);
 }
 
 struct StepBench {
