@@ -147,8 +147,10 @@ typedef struct {
   int32_t col_pipeline;       /* 1: software-pipelined column half-step kernel (1) */
   int32_t matrix_free;        /* LPs from teccl_lp_build_te apply A / A^T from the
                                  topology tables instead of the stored matrix:
-                                 0 off, 1 auto (segment kernels when K >= 16, else
-                                 per-entry), 2 per-entry, 3 segment kernels (0) */
+                                 0 off, 1 auto (stored matrix below 3M columns, where
+                                 the iteration is L2-resident; mode 4 above), 2 one
+                                 thread per entry, 3 segment kernels, 4 per-entry
+                                 columns + segment rows (1) */
   int32_t pdl;                /* 1: programmatic dependent launch between the iteration
                                  kernels (prologue of one overlaps the tail of the last) (1) */
   int32_t fused_halo;         /* row-partitioned solves: the half-step kernels store their
@@ -199,9 +201,14 @@ int teccl_lp_apply(teccl_ctx* ctx, teccl_lp* lp, int32_t transpose, int32_t matr
 /* Time the two fused PDLP iteration kernels alone (after the real scaling
  * setup), `reps` launches each, CUDA events on the context stream.
  * out6 = {ms per column-kernel launch, ms per row-kernel launch, algorithmic
- * bytes per column launch, per row launch, operator (2 matrix-free, 1 stored
- * matrix + bound dictionaries, 0 stored + bound arrays), SELL slice}. */
+ * bytes per column launch, per row launch, operator (0 stored + bound arrays,
+ * 1 stored matrix + bound dictionaries, 2/3/4 the matrix-free mode used),
+ * SELL slice}. */
 int teccl_pdlp_step_bench(teccl_ctx* ctx, teccl_lp* lp, int32_t reps, double* out6);
+/* Same with explicit options (NULL = defaults): the operator (`matrix_free`),
+ * `col_pipeline` and `pdl` select the kernels that are timed. */
+int teccl_pdlp_step_bench_opts(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* opts,
+                               int32_t reps, double* out6);
 
 /* ---------------------------------------------------------------------------
  * (4) Exact-integer schedule checker / epoch simulator for a time-expanded

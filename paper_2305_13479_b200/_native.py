@@ -22,7 +22,7 @@ EXPORTED = (
     "teccl_dist_connect", "teccl_lp_from_csr", "teccl_lp_dims",
     "teccl_lp_export", "teccl_lp_export_csc", "teccl_lp_destroy",
     "teccl_pdlp_default_opts", "teccl_pdlp_solve", "teccl_pdlp_solve_dev",
-    "teccl_spmv_bench", "teccl_pdlp_step_bench", "teccl_lp_apply", "teccl_check_te", "teccl_check_te_dev",
+    "teccl_spmv_bench", "teccl_pdlp_step_bench", "teccl_pdlp_step_bench_opts", "teccl_lp_apply", "teccl_check_te", "teccl_check_te_dev",
     "teccl_schedule_te", "teccl_schedule_fetch",
 )
 
@@ -124,6 +124,7 @@ def load(path: str | None = None):
             "teccl_pdlp_solve_dev": (C.c_int, [vp, vp, _p(PdlpOpts), vp, vp, _p(PdlpResult)]),
             "teccl_spmv_bench": (C.c_int, [vp, vp, C.c_int32, _p(C.c_double), _p(C.c_double)]),
             "teccl_pdlp_step_bench": (C.c_int, [vp, vp, C.c_int32, _p(C.c_double)]),
+            "teccl_pdlp_step_bench_opts": (C.c_int, [vp, vp, vp, C.c_int32, _p(C.c_double)]),
             "teccl_lp_apply": (C.c_int, [vp, vp, C.c_int32, C.c_int32, _p(C.c_double), _p(C.c_double),
                                          _p(C.c_double), _p(C.c_double), _p(C.c_double)]),
             "teccl_check_te": (C.c_int, [vp, _p(TeDesc), _p(C.c_double), C.c_int64, C.c_int64,

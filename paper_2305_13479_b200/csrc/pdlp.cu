@@ -58,6 +58,9 @@ constexpr int kGrid = kSMs * 8;  // blocks of the setup reduction kernels
 constexpr int kNQ = 9;           // partial quantities per check
 constexpr int kSlice = 32;
 constexpr int kTile = kThreads;  // rows (columns) per block of the step kernels
+// auto operator (matrix_free = 1): matrix-free kernels from this many columns
+// up (configs[1], 0.97M columns, runs L2-resident on the stored SELL kernels)
+constexpr int64_t kAutoMatrixFreeCols = 3000000;
 
 enum Q { Q_DX = 0, Q_DX0, Q_DY, Q_DY0, Q_RP, Q_DOBJ_ROW, Q_RD, Q_POBJ, Q_DOBJ_COL };
 
@@ -154,7 +157,7 @@ struct Vecs {
   int world, rank;
   int col_pipe;          // column half-step: pipelined resident grid (1) or one thread per column (0)
   int pdl;               // iteration kernels launched with programmatic dependent launch
-  int seg;               // matrix-free: segment-walking kernels (1) or one thread per entry (0)
+  int seg;               // matrix-free segment-walking kernels: bit 0 columns, bit 1 rows (else one thread per entry)
   Push push;             // fused halo out (see Push)
   Wait wait;             // fused halo in: neighbours' signal awaited before gathering
 };
@@ -640,6 +643,63 @@ __global__ void __launch_bounds__(kThreads) col_te_kernel(TeOp op, Vecs V, int j
       dx = (xt - xj) * (xt - xj) * w;
       dx0 = (xt - x0) * (xt - x0) * w;
     }
+  }
+  if (CHECK) {
+    double a = block_sum(dx, sh);
+    if (threadIdx.x == 0) V.part[Q_DX * V.pstride + blockIdx.x] = a;
+    a = block_sum(dx0, sh);
+    if (threadIdx.x == 0) V.part[Q_DX0 * V.pstride + blockIdx.x] = a;
+  }
+}
+
+// col_te with two adjacent columns per thread: 16-byte loads/stores of the
+// dense iterates and two independent gather chains in flight per thread
+// (HBM-resident LPs are short of bytes in flight with one column per
+// thread: profiles/r01_j_hbm_roofline.md).
+template <bool CHECK>
+__global__ void __launch_bounds__(kThreads) col_te2_kernel(TeOp op, Vecs V, int j_in_chunk) {
+  __shared__ double sh[32];
+  const uint32_t j = 2u * (blockIdx.x * kTile + threadIdx.x);
+  const bool pair = j + 1 < op.n, any = j < op.n;
+  double xj[2] = {0.0, 0.0}, x0[2] = {0.0, 0.0}, Dj[2] = {1.0, 1.0};
+  if (pair) {
+    const double2 xv = *reinterpret_cast<const double2*>(V.x + j);
+    const float2 x0v = *reinterpret_cast<const float2*>(V.x0 + j);
+    const float2 Dv = __ldg(reinterpret_cast<const float2*>(V.D + j));
+    xj[0] = xv.x; xj[1] = xv.y; x0[0] = x0v.x; x0[1] = x0v.y; Dj[0] = Dv.x; Dj[1] = Dv.y;
+  } else if (any) {
+    xj[0] = V.x[j]; x0[0] = (double)V.x0[j]; Dj[0] = (double)V.D[j];
+  }
+  pdl_wait();
+  pdl_trigger();
+  const PdlpState* st = V.st;
+  const int done = st->done;  // checked before the first store: the gathers overlap it
+  const double tau = st->tau, refl = st->refl;
+  double s[2] = {0.0, 0.0}, lb[2] = {0.0, 0.0}, ub[2] = {0.0, 0.0}, cj[2] = {0.0, 0.0};
+  if (any) s[0] = te_col(op, j, V.y, lb[0], ub[0], cj[0]);
+  if (pair) s[1] = te_col(op, j + 1, V.y, lb[1], ub[1], cj[1]);
+  if (done) return;
+  const double lam = st->lam_tab[j_in_chunk];  // chunks are at most kLamTab iterations
+  double dx = 0.0, dx0 = 0.0, xt[2], xb[2], xn[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    xt[h] = clampd(xj[h] - tau * Dj[h] * (cj[h] - s[h]), lb[h], ub[h]);
+    xb[h] = 2.0 * xt[h] - xj[h];
+    xn[h] = lam * ((1.0 + refl) * xt[h] - refl * xj[h]) + (1.0 - lam) * x0[h];
+    if (CHECK && (h == 0 ? any : pair)) {
+      const double w = 1.0 / Dj[h];
+      dx += (xt[h] - xj[h]) * (xt[h] - xj[h]) * w;
+      dx0 += (xt[h] - x0[h]) * (xt[h] - x0[h]) * w;
+    }
+  }
+  if (pair) {
+    *reinterpret_cast<double2*>(V.xbar + j) = make_double2(xb[0], xb[1]);
+    *reinterpret_cast<double2*>(V.x + j) = make_double2(xn[0], xn[1]);
+    if (CHECK) *reinterpret_cast<double2*>(V.xt + j) = make_double2(xt[0], xt[1]);
+  } else if (any) {
+    V.xbar[j] = xb[0];
+    V.x[j] = xn[0];
+    if (CHECK) V.xt[j] = xt[0];
   }
   if (CHECK) {
     double a = block_sum(dx, sh);
@@ -1327,8 +1387,10 @@ void launch_col_t(cudaStream_t st, const teccl_lp* lp, const Vecs& V, int j) {
 template <bool UNIT, bool DICT, bool CHECK>
 void launch_col(cudaStream_t st, const teccl_lp* lp, const TeOp* te, const Vecs& V, int j) {
   const bool pdl = V.pdl != 0;
-  if (te && V.seg) {
+  if (te && (V.seg & 1)) {
     launch_iter(pdl, col_seg_kernel<CHECK>, (te->n_ctask + 7) / 8, st, *te, V, j);
+  } else if (te && V.col_pipe) {  // col_pipeline selects the two-column variant
+    launch_iter(pdl, col_te2_kernel<CHECK>, (int)((te->n + 2 * kTile - 1) / (2 * kTile)), st, *te, V, j);
   } else if (te) {
     launch_iter(pdl, col_te_kernel<CHECK>, (int)((te->n + kTile - 1) / kTile), st, *te, V, j);
   } else if (V.push.n || V.wait.npeer) {  // fused peer exchange compiled in only where used
@@ -1340,7 +1402,7 @@ void launch_col(cudaStream_t st, const teccl_lp* lp, const TeOp* te, const Vecs&
 template <bool UNIT, bool DICT, bool CHECK>
 void launch_row(cudaStream_t st, const teccl_lp* lp, const TeOp* te, const Vecs& V, int j) {
   const bool pdl = V.pdl != 0;
-  if (te && V.seg) launch_iter(pdl, row_seg_kernel<CHECK>, (te->n_rtask + 7) / 8, st, *te, V, j);
+  if (te && (V.seg & 2)) launch_iter(pdl, row_seg_kernel<CHECK>, (te->n_rtask + 7) / 8, st, *te, V, j);
   else if (te) launch_iter(pdl, row_te_kernel<CHECK>, (int)((te->m + kTile - 1) / kTile), st, *te, V, j);
   else if (V.push.n || V.wait.npeer)
     launch_iter(pdl, row_step_kernel<UNIT, DICT, CHECK, true>, V.nb_row, st, (int32_t)lp->m, row_view(lp), V, j);
@@ -1351,6 +1413,7 @@ void launch_row(cudaStream_t st, const teccl_lp* lp, const TeOp* te, const Vecs&
 struct StepBench {
   int reps;
   double ms_col, ms_row, bytes_col, bytes_row;
+  int matrix_free;  // out: the operator the timed kernels used
 };
 
 // Exchange plumbing of one solve: peer-memory halo/reduction events for a
@@ -1523,10 +1586,17 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
   TECCL_CUDA(cudaMemsetAsync(yt_w, 0, sizeof(double) * (nrw + 1), st));
   // matrix-free operator for single-device TE LPs; the SELL copies are
   // only built for LPs that need them
-  const TeOp* te = (o->matrix_free && lp->te && lp->part_world == 1) ? &((TeHold*)lp->te)->op : nullptr;
-  // segment kernels unless per-entry is asked for (2) or the segments are
-  // too short to fill a warp task (auto, K < 16)
-  const bool seg = te && (o->matrix_free == 3 || (o->matrix_free == 1 && te->K >= 16));
+  // Operator per half-step: 0 stored SELL, 2 matrix-free one thread per
+  // entry, 3 matrix-free segment tasks on both sides, 4 per-entry columns +
+  // segment rows. 1 (auto): the stored SELL kernels while the iteration's
+  // working set is L2-resident (latency-bound, profiles/r01_h), mode 4 above
+  // that (HBM-bound: no index stream, fastest pair measured on 4-, 8- and
+  // 16-chassis LPs, profiles/r01_j_hbm_roofline.md).
+  const TeOp* te_all = (lp->te && lp->part_world == 1) ? &((TeHold*)lp->te)->op : nullptr;
+  int mf = te_all ? o->matrix_free : 0;
+  if (mf == 1) mf = (lp->n >= kAutoMatrixFreeCols && te_all->K >= 16) ? 4 : 0;
+  const TeOp* te = mf ? te_all : nullptr;
+  const bool seg_col = mf == 3, seg_row = mf == 3 || mf == 4;
   if (!te) {
     int rc = teccl_build_sell(lp, st);
     if (rc) return rc;
@@ -1663,13 +1733,11 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
   V.rank = rank;
   V.col_pipe = o->col_pipeline;
   V.pdl = o->pdl;
-  V.seg = seg ? 1 : 0;
+  V.seg = (seg_col ? 1 : 0) | (seg_row ? 2 : 0);
   // partial-sum slots: the iteration kernels write one per block; the
   // reduction reads max(blocks) slots per quantity (unwritten ones stay 0)
-  if (seg) {
-    V.nb_col = std::max(V.nb_col, (te->n_ctask + 7) / 8);
-    V.nb_row = std::max(V.nb_row, (te->n_rtask + 7) / 8);
-  }
+  if (seg_col) V.nb_col = std::max(V.nb_col, (te->n_ctask + 7) / 8);
+  if (seg_row) V.nb_row = std::max(V.nb_row, (te->n_rtask + 7) / 8);
   // Vc: column kernels (own x side, gather y windows); Vr: row kernels
   // (own y side, gather x windows); Vi: owned parts only
   Vecs Vc = V, Vr = V, Vi = V;
@@ -1712,6 +1780,7 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
     sb->ms_row = m2 / sb->reps;
     // algorithmic bytes: SELL slice headers and every
     // stored entry once, the gathered vector once, dense operands once
+    sb->matrix_free = mf;
     if (te) {  // no stored matrix: dense vectors, the gathered operand once, capacities
       sb->bytes_col = 8.0 * nrw + 32.0 * n;
       sb->bytes_row = 8.0 * ncw + 24.0 * m + 8.0 * (double)te->EK;
@@ -1730,7 +1799,7 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
   }
 
   // --- chunk graph (captured once per LP and chunk length)
-  const int graph_key = chunk * 64 + (o->col_pipeline ? 1 : 0) + (te ? 2 : 0) + (o->pdl ? 4 : 0) + (seg ? 8 : 0) + 16 * o->fused_halo;
+  const int graph_key = chunk * 256 + (o->col_pipeline ? 1 : 0) + (te ? 2 : 0) + (o->pdl ? 4 : 0) + 8 * V.seg + 32 * o->fused_halo;
   if (o->use_graphs && W.gexec && W.graph_chunk != graph_key) {
     cudaGraphExecDestroy(W.gexec);
     W.gexec = nullptr;
@@ -1872,7 +1941,7 @@ extern "C" void teccl_pdlp_default_opts(teccl_pdlp_opts* o) {
   o->omega_ki = 0.0;
   o->omega_kd = 0.0;
   o->col_pipeline = 1;
-  o->matrix_free = 0;  // measured: the SELL kernels are faster on configs[1] (profiles/r01_h)
+  o->matrix_free = 1;  // auto: stored SELL while L2-resident (configs[1]), matrix-free above
   o->pdl = 1;
   o->fused_halo = 1;
 }
@@ -1915,23 +1984,29 @@ extern "C" int teccl_pdlp_solve(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_o
   return rc;
 }
 
-extern "C" int teccl_pdlp_step_bench(teccl_ctx* ctx, teccl_lp* lp, int32_t reps, double* out6) {
+extern "C" int teccl_pdlp_step_bench_opts(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* opts,
+                                          int32_t reps, double* out6) {
   if (!ctx || !lp || reps < 1 || !out6) { set_error("bad argument"); return TECCL_EINVAL; }
   TECCL_CUDA(cudaSetDevice(ctx->device));
   teccl_pdlp_opts o;
-  teccl_pdlp_default_opts(&o);
+  if (opts) o = *opts; else teccl_pdlp_default_opts(&o);
   teccl_pdlp_result res{};
   double* xd = nullptr;
   TECCL_CUDA(cudaMallocAsync((void**)&xd, sizeof(double) * (lp->n + 1), ctx->stream));
-  StepBench sb{reps, 0, 0, 0, 0};
+  StepBench sb{reps, 0, 0, 0, 0, 0};
   int rc = dispatch(ctx, lp, &o, xd, nullptr, &res, &sb);
   cudaFreeAsync(xd, ctx->stream);
   TECCL_CUDA(cudaStreamSynchronize(ctx->stream));
   out6[0] = sb.ms_col; out6[1] = sb.ms_row; out6[2] = sb.bytes_col; out6[3] = sb.bytes_row;
-  // operator: 2 matrix-free, 1 stored matrix + bound-class dictionaries, 0 stored + arrays
-  out6[4] = (o.matrix_free && lp->te && lp->part_world == 1) ? 2.0 : (lp->col_code && lp->row_code) ? 1.0 : 0.0;
+  // operator: 0 stored + bound arrays, 1 stored + bound-class dictionaries,
+  // 2/3/4 matrix-free (teccl_pdlp_opts.matrix_free modes)
+  out6[4] = sb.matrix_free ? (double)sb.matrix_free : (lp->col_code && lp->row_code) ? 1.0 : 0.0;
   out6[5] = (double)kSlice;
   return rc;
+}
+
+extern "C" int teccl_pdlp_step_bench(teccl_ctx* ctx, teccl_lp* lp, int32_t reps, double* out6) {
+  return teccl_pdlp_step_bench_opts(ctx, lp, nullptr, reps, out6);
 }
 
 namespace teccl {

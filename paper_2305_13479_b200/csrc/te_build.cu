@@ -708,6 +708,19 @@ int te_op_tables(const teccl_te_desc* desc, TeHold* h, cudaStream_t st) {
   for (int p = 0; p < P; ++p) add(rt, SEG_CUM, p, 0, (int64_t)o.R_cum + (int64_t)p * K, K);
   if (o.has_bcap)
     for (int g = 0; g < G; ++g) add(rt, SEG_BCAP, 0, g, (int64_t)o.R_bcap + (int64_t)g * (K + 1), K + 1);
+  // Epoch-tile-major task order: every family's tasks for epochs
+  // [64t, 64t + 64) run next to each other, so the gathered vector is
+  // touched by all its rows (columns) within a window of a few epoch tiles
+  // and is read from HBM once per half-step instead of once per family
+  // pass (x-bar is read by the capacity rows and again by two conservation
+  // rows per flow column).
+  auto tile = [](const int4& t) {
+    const int kind = t.x & 15, off = t.w & 0xffffff;
+    return kind == SEG_P ? off / (2 * kSegTask) : off / kSegTask;
+  };
+  auto by_tile = [&](const int4& a, const int4& b) { return tile(a) < tile(b); };
+  std::stable_sort(ct.begin(), ct.end(), by_tile);
+  std::stable_sort(rt.begin(), rt.end(), by_tile);
   std::vector<double> ninv(K);
   for (int64_t k = 0; k < K; ++k) ninv[k] = -1.0 / (double)(k + 1);
   int4* d4 = nullptr; int2* ds = nullptr; int2* di = nullptr;

@@ -258,12 +258,21 @@ class DeviceLP:
             del out["cost"]
         return out
 
-    def step_bench(self, reps: int = 50) -> dict:
-        """Per-launch device time and algorithmic bytes of the fused kernels."""
+    def step_bench(self, reps: int = 50, pdlp: dict | None = None) -> dict:
+        """Per-launch device time and algorithmic bytes of the fused kernels;
+        `pdlp` overrides teccl_pdlp_opts fields (e.g. {"matrix_free": 2})."""
         out = (C.c_double * 6)()
-        nat.check(self.ctx.lib.teccl_pdlp_step_bench(self.ctx.handle, self.handle, int(reps), out))
+        if pdlp:
+            o = nat.PdlpOpts()
+            self.ctx.lib.teccl_pdlp_default_opts(C.byref(o))
+            for k, v in pdlp.items():
+                setattr(o, k, type(getattr(o, k))(v))
+            nat.check(self.ctx.lib.teccl_pdlp_step_bench_opts(self.ctx.handle, self.handle, C.byref(o),
+                                                              int(reps), out))
+        else:
+            nat.check(self.ctx.lib.teccl_pdlp_step_bench(self.ctx.handle, self.handle, int(reps), out))
         return {"ms_col": out[0], "ms_row": out[1], "bytes_col": out[2], "bytes_row": out[3],
-                "dict": out[4] >= 1.0, "matrix_free": out[4] == 2.0,
+                "dict": out[4] == 1.0, "matrix_free": int(out[4]) if out[4] >= 2.0 else 0,
                 "slice": int(out[5])}
 
     def close(self) -> None:
