@@ -50,6 +50,12 @@ namespace teccl {
 #ifndef TECCL_ROW_MINB
 #define TECCL_ROW_MINB 5   // __launch_bounds__ min blocks per SM (48 registers)
 #endif
+#ifndef TECCL_SEG_MINB
+#define TECCL_SEG_MINB 6   // same, row segment kernel (40 registers: -28 % on the 8-chassis LP)
+#endif
+#ifndef TECCL_TE2_MINB
+#define TECCL_TE2_MINB 8   // same, two-column column kernel (32 registers: -8 % on the 16-chassis LP)
+#endif
 #ifndef TECCL_COL_MINB
 #define TECCL_COL_MINB 4   // same, pipelined column kernel (64 registers: measured best)
 #endif
@@ -657,7 +663,7 @@ __global__ void __launch_bounds__(kThreads) col_te_kernel(TeOp op, Vecs V, int j
 // (HBM-resident LPs are short of bytes in flight with one column per
 // thread: profiles/r01_j_hbm_roofline.md).
 template <bool CHECK>
-__global__ void __launch_bounds__(kThreads) col_te2_kernel(TeOp op, Vecs V, int j_in_chunk) {
+__global__ void __launch_bounds__(kThreads, TECCL_TE2_MINB) col_te2_kernel(TeOp op, Vecs V, int j_in_chunk) {
   __shared__ double sh[32];
   const uint32_t j = 2u * (blockIdx.x * kTile + threadIdx.x);
   const bool pair = j + 1 < op.n, any = j < op.n;
@@ -804,7 +810,7 @@ __global__ void __launch_bounds__(kThreads) col_seg_kernel(TeOp op, Vecs V, int 
 }
 
 template <bool CHECK>
-__global__ void __launch_bounds__(kThreads) row_seg_kernel(TeOp op, Vecs V, int j_in_chunk) {
+__global__ void __launch_bounds__(kThreads, TECCL_SEG_MINB) row_seg_kernel(TeOp op, Vecs V, int j_in_chunk) {
   __shared__ double sh[32];
   const int wi = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   const int4 tk = (wi < op.n_rtask) ? __ldg(op.rtask + wi) : make_int4(0, 0, 0, 0);
