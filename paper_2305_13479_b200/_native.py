@@ -80,6 +80,7 @@ class CheckReport(C.Structure):
 
 _lib = None
 _lock = threading.Lock()
+_ctx_lock = threading.Lock()
 
 
 def load(path: str | None = None):
@@ -170,10 +171,13 @@ class Context:
         self.device = device
 
     @classmethod
-    def get(cls, device: int = 0) -> "Context":
-        ctx = cls._cache.get(device)
-        if ctx is None:
-            ctx = cls._cache[device] = Context(device)
+    def get(cls, device: int = 0, slot: int = 0) -> "Context":
+        """Context `slot` of `device` (slot > 0: extra streams for concurrent
+        independent solves on one GPU)."""
+        with _ctx_lock:
+            ctx = cls._cache.get((device, slot))
+            if ctx is None:
+                ctx = cls._cache[(device, slot)] = Context(device)
         return ctx
 
     def sync(self) -> None:

@@ -16,6 +16,10 @@
 namespace teccl {
 static thread_local std::string g_err;
 void set_error(const std::string& msg) { g_err = msg; }
+std::mutex& device_mutex() {
+  static std::mutex mu;
+  return mu;
+}
 }  // namespace teccl
 
 using namespace teccl;
@@ -260,7 +264,7 @@ extern "C" int teccl_lp_export(const teccl_lp* lp, int64_t* row_ptr, int32_t* co
                                double* obj) {
   if (!lp) { set_error("null lp"); return TECCL_EINVAL; }
   TECCL_CUDA(cudaSetDevice(lp->device));
-  TECCL_CUDA(cudaDeviceSynchronize());
+  if (lp->stream) TECCL_CUDA(cudaStreamSynchronize(lp->stream));
   int rc = export_matrix(lp, false, row_ptr, col, val);
   if (rc) return rc;
   if (row_lo) TECCL_CUDA(cudaMemcpy(row_lo, lp->row_lo, lp->m * sizeof(double), cudaMemcpyDeviceToHost));
@@ -274,14 +278,19 @@ extern "C" int teccl_lp_export(const teccl_lp* lp, int64_t* row_ptr, int32_t* co
 extern "C" int teccl_lp_export_csc(const teccl_lp* lp, int64_t* col_ptr, int32_t* row, double* val) {
   if (!lp) { set_error("null lp"); return TECCL_EINVAL; }
   TECCL_CUDA(cudaSetDevice(lp->device));
-  TECCL_CUDA(cudaDeviceSynchronize());
+  if (lp->stream) TECCL_CUDA(cudaStreamSynchronize(lp->stream));
   return export_matrix(lp, true, col_ptr, row, val);
 }
 
 extern "C" int teccl_lp_destroy(teccl_lp* lp) {
   if (!lp) return TECCL_OK;
   cudaSetDevice(lp->device);
-  cudaDeviceSynchronize();
+  if (lp->stream) {
+    cudaStreamSynchronize(lp->stream);
+  } else {
+    std::lock_guard<std::mutex> lock(device_mutex());
+    cudaDeviceSynchronize();
+  }
   if (lp->pdlp_ws && lp->ws_free) lp->ws_free(lp->pdlp_ws);
   if (lp->dist && lp->dist_free) lp->dist_free(lp->dist);
   if (lp->te && lp->te_free) lp->te_free(lp->te);
@@ -290,11 +299,15 @@ extern "C" int teccl_lp_destroy(teccl_lp* lp) {
                   lp->srow_off, lp->srow_w, lp->sell_idx, lp->srow_val,
                   lp->scol_off, lp->scol_w, lp->scol_val,
                   lp->col_code, lp->row_code, lp->col_dict, lp->row_dict};
-  for (void* p : ptrs)
-    if (p) {
-      if (lp->stream) cudaFreeAsync(p, lp->stream);
-      else cudaFree(p);
-    }
+  {
+    std::unique_lock<std::mutex> lock(device_mutex(), std::defer_lock);
+    if (!lp->stream) lock.lock();  // cudaFree synchronises the device
+    for (void* p : ptrs)
+      if (p) {
+        if (lp->stream) cudaFreeAsync(p, lp->stream);
+        else cudaFree(p);
+      }
+  }
   if (lp->stream) cudaStreamSynchronize(lp->stream);
   delete lp;
   return TECCL_OK;

@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <mutex>
 #include <string>
 
 #include "../../include/teccl_b200.h"
@@ -19,6 +20,13 @@ constexpr uint32_t kSignBit = 0x80000000u;  // unit-coefficient CSR: bit31 = neg
 constexpr uint32_t kIdxMask = 0x7fffffffu;
 
 void set_error(const std::string& msg);
+
+// Held around CUDA-graph capture and around calls that synchronise the
+// whole device (pinned-host alloc/free, device-wide syncs): several host
+// threads may drive their own contexts on one GPU (sweep.solve_shard), and a
+// device-wide synchronisation issued while another thread captures
+// invalidates that capture.
+std::mutex& device_mutex();
 
 #define TECCL_CUDA(call)                                                         \
   do {                                                                           \

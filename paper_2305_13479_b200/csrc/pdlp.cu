@@ -1310,9 +1310,10 @@ struct Workspace {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   ~Workspace() {
     cudaSetDevice(device);
-    cudaDeviceSynchronize();
+    cudaStreamSynchronize(st);  // every use of the workspace was on st
     for (void* p : bufs) cudaFreeAsync(p, st);
     cudaStreamSynchronize(st);
+    std::lock_guard<std::mutex> lock(device_mutex());
     if (gexec) cudaGraphExecDestroy(gexec);
     if (ring) cudaFreeHost(ring);
     for (auto e : evs) cudaEventDestroy(e);
@@ -1814,6 +1815,7 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
   X.nl = 0;
   int64_t per_chunk = 0;
   if (o->use_graphs && !W.gexec) {
+    std::lock_guard<std::mutex> capture_lock(device_mutex());
     cudaGraph_t g;
     cudaStream_t cap;
     TECCL_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
@@ -1832,6 +1834,7 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
   // --- iterate: chunks queued `lookahead` deep; the device stops itself
   const int look = o->lookahead > 0 ? o->lookahead : 1;
   if (W.ring_len < look) {
+    std::lock_guard<std::mutex> lock(device_mutex());
     if (W.ring) cudaFreeHost(W.ring);
     W.ring = nullptr;
     TECCL_CUDA(cudaMallocHost((void**)&W.ring, sizeof(PdlpState) * look));
@@ -1886,7 +1889,8 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
     TECCL_CUDA(cudaMemcpyAsync(&dst->done, &kStopped, sizeof(int), cudaMemcpyHostToDevice, st));
   }
   TECCL_CUDA(cudaStreamSynchronize(st));
-  TECCL_CUDA(cudaMemcpy(&last, dst, sizeof(PdlpState), cudaMemcpyDeviceToHost));
+  TECCL_CUDA(cudaMemcpyAsync(&last, dst, sizeof(PdlpState), cudaMemcpyDeviceToHost, st));
+  TECCL_CUDA(cudaStreamSynchronize(st));
   if (last.done == 1) status = TECCL_OPTIMAL;
   if (last.done == 3) last.done = 0;
 

@@ -288,14 +288,15 @@ class DeviceLP:
 
 
 def build_lp_model(t, d, cfg: EpochConfig, opts: ModelOptions | None = None,
-                   device: int = 0) -> DeviceLP:
-    """Build the copy-free TE-CCL LP on the GPU (reference lp.py:22-136)."""
+                   device: int = 0, slot: int = 0) -> DeviceLP:
+    """Build the copy-free TE-CCL LP on the GPU (reference lp.py:22-136);
+    `slot` selects the device's context / stream (concurrent solves)."""
     plan = make_plan(t, d, cfg, opts)
-    return build_from_plan(plan, device)
+    return build_from_plan(plan, device, slot)
 
 
-def build_from_plan(plan: LpPlan, device: int = 0) -> DeviceLP:
-    ctx = nat.Context.get(device)
+def build_from_plan(plan: LpPlan, device: int = 0, slot: int = 0) -> DeviceLP:
+    ctx = nat.Context.get(device, slot)
     h = C.c_void_p()
     nat.check(ctx.lib.teccl_lp_build_te(ctx.handle, C.byref(plan.desc()), C.byref(h)))
     return DeviceLP(h, ctx, plan, name="lp-alltoall")

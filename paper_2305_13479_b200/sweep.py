@@ -54,12 +54,12 @@ def build_instance(inst: Instance):
     return t, d, EpochConfig(tau, inst.K, "fastest", inst.em, d.chunk_size)
 
 
-def solve_instance(inst: Instance, device: int = 0, eps_rel: float = 1e-4) -> dict:
+def solve_instance(inst: Instance, device: int = 0, eps_rel: float = 1e-4, slot: int = 0) -> dict:
     from .lp import build_lp_model, lp_completion_epoch
     from .solver import SolverOptions, solve
     t, d, cfg = build_instance(inst)
     t0 = time.perf_counter()
-    lp = build_lp_model(t, d, cfg, device=device)
+    lp = build_lp_model(t, d, cfg, device=device, slot=slot)
     sol = solve(lp, SolverOptions(eps_rel=eps_rel, device=device))
     rec = {"instance": asdict(inst), "status": sol.status, "objective": sol.objective,
            "iters": sol.meta["iters"], "device_seconds": sol.meta["device_seconds"],
@@ -75,12 +75,50 @@ def solve_instance(inst: Instance, device: int = 0, eps_rel: float = 1e-4) -> di
     return rec
 
 
+def solve_shard(items: list, device: int, solver, streams: int = 1) -> list:
+    """Solve (index, instance) pairs on one GPU. streams > 1: that many host
+    threads, each driving its own context (CUDA stream) on the device, take
+    instances from a shared queue -- small LPs are launch/latency-bound, so
+    concurrent solves fill the GPU that one solve leaves idle. Records come
+    back in input order."""
+    if streams <= 1 or len(items) <= 1:
+        return [(i, solver(inst, device)) for i, inst in items]
+    import queue
+    import threading
+    q = queue.Queue()
+    for it in items:
+        q.put(it)
+    out, errs = {}, []
+
+    def work(slot):
+        while True:
+            try:
+                i, inst = q.get_nowait()
+            except queue.Empty:
+                return
+            try:
+                out[i] = solver(inst, device, slot=slot)
+            except Exception as exc:  # surfaced after the join
+                errs.append(exc)
+                return
+
+    threads = [threading.Thread(target=work, args=(k,)) for k in range(min(streams, len(items)))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    if errs:
+        raise errs[0]
+    return [(i, out[i]) for i, _ in items]
+
+
 def run_sweep(instances: list[Instance], rank: int = 0, world: int = 1, device: int = 0,
-              solver=solve_instance, group=None) -> list[dict]:
-    """Solve this rank's shard; with world > 1 gather every record on every
-    rank (ordered like `instances`)."""
-    mine = [(i, solver(inst, device)) for i, inst in
-            zip(range(rank, len(instances), world), shard(instances, rank, world))]
+              solver=solve_instance, group=None, streams: int = 1) -> list[dict]:
+    """Solve this rank's shard (`streams` concurrent solves on the rank's
+    GPU); with world > 1 gather every record on every rank (ordered like
+    `instances`)."""
+    mine = solve_shard(list(zip(range(rank, len(instances), world), shard(instances, rank, world))),
+                       device, solver, streams)
     if world == 1:
         return [r for _, r in mine]
     import torch.distributed as dist

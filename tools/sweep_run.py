@@ -23,14 +23,15 @@ solve_instance(insts[0], device=local)  # warm-up: context, module load
 if world > 1:
     dist.barrier()
 t0 = time.perf_counter()
-recs = run_sweep(insts, rank, world, device=local)
+streams = int(os.environ.get("STREAMS", "8"))
+recs = run_sweep(insts, rank, world, device=local, streams=streams)
 el = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=f"cuda:{local}")
 if world > 1:
     dist.all_reduce(el, op=dist.ReduceOp.MAX)
 if rank == 0:
     ok = sum(r["status"] == "optimal" for r in recs)
     print(json.dumps({"workload": "configs[3] sweep: 64 single-chassis NDv2 LPs (4 chunk sizes x 4 EM x 2 "
-                      "collectives x 2 chunk counts)", "n_gpus": world, "lps": len(recs), "optimal": ok,
+                      "collectives x 2 chunk counts)", "n_gpus": world, "streams_per_gpu": streams, "lps": len(recs), "optimal": ok,
                       "seconds_max_over_ranks": float(el), "lps_per_s": len(recs) / float(el),
                       "iters_total": sum(r["iters"] for r in recs)}), flush=True)
 if world > 1:
