@@ -150,7 +150,9 @@ typedef struct {
                                  0 off, 1 auto (stored matrix below 3M columns, where
                                  the iteration is L2-resident; mode 4 above), 2 one
                                  thread per entry, 3 segment kernels, 4 per-entry
-                                 columns + segment rows (1) */
+                                 columns + segment rows (1). Blocks of row-partitioned
+                                 LPs: 2-4 select the epoch-major matrix-free operator,
+                                 auto the stored matrix */
   int32_t pdl;                /* 1: programmatic dependent launch between the iteration
                                  kernels (prologue of one overlaps the tail of the last) (1) */
   int32_t fused_halo;         /* row-partitioned solves: the half-step kernels store their

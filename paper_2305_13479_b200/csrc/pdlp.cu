@@ -753,6 +753,96 @@ __global__ void __launch_bounds__(kThreads) row_te_kernel(TeOp op, Vecs V, int j
   }
 }
 
+// Matrix-free half-steps of one rank's epoch block (te_gen.cuh em_col /
+// em_row): the col_step / row_step updates with A^T y and A x evaluated from
+// the topology tables in the epoch-major window, including the fused peer
+// exchange of row-partitioned solves (PEER).
+template <bool CHECK, bool PEER>
+__global__ void __launch_bounds__(kThreads) col_em_kernel(EmOp op, Vecs V, int j_in_chunk) {
+  __shared__ double sh[32];
+  const uint32_t j = blockIdx.x * kTile + threadIdx.x;
+  double xj = 0.0, x0 = 0.0, Dj = 1.0, lb = 0.0, ub = 0.0, cj = 0.0, s = 0.0;
+  if (j < op.n) {
+    xj = V.x[j];
+    x0 = (double)V.x0[j];
+    Dj = (double)V.D[j];
+  }
+  pdl_wait();
+  pdl_trigger();
+  const PdlpState* st = V.st;
+  const int done = st->done;  // checked before the first store: the gathers overlap it
+  const double tau = st->tau, refl = st->refl;
+  if (PEER && V.wait.npeer && (done || !block_wait_peers(V.wait, V.st))) return;
+  if (j < op.n) s = em_col(op, j, V.y, lb, ub, cj);
+  if (done) return;
+  const double lam = st->lam_tab[j_in_chunk];  // chunks are at most kLamTab iterations
+  bool wrote = false;
+  double dx = 0.0, dx0 = 0.0;
+  if (j < op.n) {
+    const double xt = clampd(xj - tau * Dj * (cj - s), lb, ub);
+    const double xb = 2.0 * xt - xj;
+    V.xbar[j] = xb;
+    wrote = PEER && push_entry<CHECK>(V.push, j, xb, xt);
+    V.x[j] = lam * ((1.0 + refl) * xt - refl * xj) + (1.0 - lam) * x0;
+    if (CHECK) {
+      V.xt[j] = xt;
+      const double w = 1.0 / Dj;
+      dx = (xt - xj) * (xt - xj) * w;
+      dx0 = (xt - x0) * (xt - x0) * w;
+    }
+  }
+  if (CHECK) {
+    double a = block_sum(dx, sh);
+    if (threadIdx.x == 0) V.part[Q_DX * V.pstride + blockIdx.x] = a;
+    a = block_sum(dx0, sh);
+    if (threadIdx.x == 0) V.part[Q_DX0 * V.pstride + blockIdx.x] = a;
+  }
+  if (PEER) push_signal(V.push, wrote);
+}
+
+template <bool CHECK, bool PEER>
+__global__ void __launch_bounds__(kThreads) row_em_kernel(EmOp op, Vecs V, int j_in_chunk) {
+  __shared__ double sh[32];
+  const uint32_t i = blockIdx.x * kTile + threadIdx.x;
+  double yi = 0.0, y0 = 0.0, Ei = 1.0, lo = 0.0, hi = 0.0, s = 0.0;
+  if (i < op.m) {
+    yi = V.y[i];
+    y0 = (double)V.y0[i];
+    Ei = (double)V.E[i];
+  }
+  pdl_wait();
+  pdl_trigger();
+  const PdlpState* st = V.st;
+  const int done = st->done;  // checked before the first store: the gathers overlap it
+  const double sigma = st->sigma, refl = st->refl;
+  if (PEER && V.wait.npeer && (done || !block_wait_peers(V.wait, V.st))) return;
+  if (i < op.m) s = em_row(op, i, V.xbar, lo, hi);
+  if (done) return;
+  const double lam = st->lam_tab[j_in_chunk];  // chunks are at most kLamTab iterations
+  bool wrote = false;
+  double dy = 0.0, dy0 = 0.0;
+  if (i < op.m) {
+    const double se = sigma * Ei;
+    const double yt = yi - se * (s - clampd(s - yi / se, lo, hi));
+    const double yn = lam * ((1.0 + refl) * yt - refl * yi) + (1.0 - lam) * y0;
+    V.y[i] = yn;
+    wrote = PEER && push_entry<CHECK>(V.push, i, yn, yt);
+    if (CHECK) {
+      V.yt[i] = yt;
+      const double w = 1.0 / Ei;
+      dy = (yt - yi) * (yt - yi) * w;
+      dy0 = (yt - y0) * (yt - y0) * w;
+    }
+  }
+  if (CHECK) {
+    double a = block_sum(dy, sh);
+    if (threadIdx.x == 0) V.part[Q_DY * V.pstride + blockIdx.x] = a;
+    a = block_sum(dy0, sh);
+    if (threadIdx.x == 0) V.part[Q_DY0 * V.pstride + blockIdx.x] = a;
+  }
+  if (PEER) push_signal(V.push, wrote);
+}
+
 // Segment-walking half-steps (te_gen.cuh seg_cols / seg_rows): one warp per
 // task of up to 64 consecutive entries of one column / row family, so the
 // table lookups are per task and each entry costs only its gathers and the
@@ -863,15 +953,17 @@ __global__ void __launch_bounds__(kThreads, TECCL_SEG_MINB) row_seg_kernel(TeOp 
 
 // KKT over rows at T(z) = (xt, yt): primal residual of A.xt against the row
 // bounds and the row part of the dual objective.
-template <bool UNIT, bool TE>
-__global__ void __launch_bounds__(kThreads) kkt_row_kernel(int32_t m, SellView S, TeOp op, Vecs V) {
+template <bool UNIT, int OPK>  // operator: 0 stored SELL, 1 TeOp, 2 EmOp
+__global__ void __launch_bounds__(kThreads) kkt_row_kernel(int32_t m, SellView S, TeOp op, EmOp em, Vecs V) {
   __shared__ double sh[32];
   if (V.st->done) return;
   const int64_t i = (int64_t)blockIdx.x * kTile + threadIdx.x;
   double lo = 0.0, hi = 0.0, s = 0.0;
   if (i < m) {
-    if (TE) {
+    if (OPK == 1) {
       s = te_row(op, (uint32_t)i, V.xt, lo, hi);
+    } else if (OPK == 2) {
+      s = em_row(em, (uint32_t)i, V.xt, lo, hi);
     } else {
       s = sell_dot<UNIT, 8>(S, i, V.xt);
       lo = V.lo_u[i];
@@ -894,15 +986,17 @@ __global__ void __launch_bounds__(kThreads) kkt_row_kernel(int32_t m, SellView S
 
 // KKT over columns: reduced costs, dual residual, primal objective and the
 // bound part of the dual objective.
-template <bool UNIT, bool TE>
-__global__ void __launch_bounds__(kThreads) kkt_col_kernel(int32_t n, SellView S, TeOp op, Vecs V) {
+template <bool UNIT, int OPK>
+__global__ void __launch_bounds__(kThreads) kkt_col_kernel(int32_t n, SellView S, TeOp op, EmOp em, Vecs V) {
   __shared__ double sh[32];
   if (V.st->done) return;
   const int64_t j = (int64_t)blockIdx.x * kTile + threadIdx.x;
   double lb = 0.0, ub = 0.0, cj = 0.0, s = 0.0;
   if (j < n) {
-    if (TE) {
+    if (OPK == 1) {
       s = te_col(op, (uint32_t)j, V.yt, lb, ub, cj);
+    } else if (OPK == 2) {
+      s = em_col(em, (uint32_t)j, V.yt, lb, ub, cj);
     } else {
       s = sell_dot<UNIT>(S, j, V.yt);
       cj = V.c_u[j];
@@ -1392,9 +1486,13 @@ void launch_col_t(cudaStream_t st, const teccl_lp* lp, const Vecs& V, int j) {
   }
 }
 template <bool UNIT, bool DICT, bool CHECK>
-void launch_col(cudaStream_t st, const teccl_lp* lp, const TeOp* te, const Vecs& V, int j) {
+void launch_col(cudaStream_t st, const teccl_lp* lp, const TeOp* te, const EmOp* em, const Vecs& V, int j) {
   const bool pdl = V.pdl != 0;
-  if (te && (V.seg & 1)) {
+  if (em) {
+    const int g = (int)((em->n + kTile - 1) / kTile);
+    if (V.push.n || V.wait.npeer) launch_iter(pdl, col_em_kernel<CHECK, true>, g, st, *em, V, j);
+    else launch_iter(pdl, col_em_kernel<CHECK, false>, g, st, *em, V, j);
+  } else if (te && (V.seg & 1)) {
     launch_iter(pdl, col_seg_kernel<CHECK>, (te->n_ctask + 7) / 8, st, *te, V, j);
   } else if (te && V.col_pipe) {  // col_pipeline selects the two-column variant
     launch_iter(pdl, col_te2_kernel<CHECK>, (int)((te->n + 2 * kTile - 1) / (2 * kTile)), st, *te, V, j);
@@ -1407,9 +1505,13 @@ void launch_col(cudaStream_t st, const teccl_lp* lp, const TeOp* te, const Vecs&
   }
 }
 template <bool UNIT, bool DICT, bool CHECK>
-void launch_row(cudaStream_t st, const teccl_lp* lp, const TeOp* te, const Vecs& V, int j) {
+void launch_row(cudaStream_t st, const teccl_lp* lp, const TeOp* te, const EmOp* em, const Vecs& V, int j) {
   const bool pdl = V.pdl != 0;
-  if (te && (V.seg & 2)) launch_iter(pdl, row_seg_kernel<CHECK>, (te->n_rtask + 7) / 8, st, *te, V, j);
+  if (em) {
+    const int g = (int)((em->m + kTile - 1) / kTile);
+    if (V.push.n || V.wait.npeer) launch_iter(pdl, row_em_kernel<CHECK, true>, g, st, *em, V, j);
+    else launch_iter(pdl, row_em_kernel<CHECK, false>, g, st, *em, V, j);
+  } else if (te && (V.seg & 2)) launch_iter(pdl, row_seg_kernel<CHECK>, (te->n_rtask + 7) / 8, st, *te, V, j);
   else if (te) launch_iter(pdl, row_te_kernel<CHECK>, (int)((te->m + kTile - 1) / kTile), st, *te, V, j);
   else if (V.push.n || V.wait.npeer)
     launch_iter(pdl, row_step_kernel<UNIT, DICT, CHECK, true>, V.nb_row, st, (int32_t)lp->m, row_view(lp), V, j);
@@ -1453,21 +1555,21 @@ struct Exchange {
 };
 
 template <bool UNIT, bool DICT>
-void enqueue_chunk(int chunk, cudaStream_t st, const teccl_lp* lp, const TeOp* te, const Vecs& Vc, const Vecs& Vr,
+void enqueue_chunk(int chunk, cudaStream_t st, const teccl_lp* lp, const TeOp* te, const EmOp* em, const Vecs& Vc, const Vecs& Vr,
                    Exchange& X, double* y_w, double* yt_w) {
   const int64_t nrw = gather_rows(lp), orr = own_row_off(lp);
   for (int j = 0; j < chunk; ++j) {
     const bool check = (j == chunk - 1);
-    if (check) launch_col<UNIT, DICT, true>(st, lp, te, Vc, j);
-    else launch_col<UNIT, DICT, false>(st, lp, te, Vc, j);
+    if (check) launch_col<UNIT, DICT, true>(st, lp, te, em, Vc, j);
+    else launch_col<UNIT, DICT, false>(st, lp, te, em, Vc, j);
     if (!Vc.push.n) {  // fused kernels push their own halos
       if (check) X.halo(st, {A_XBAR, A_XT});
       else X.halo(st, {A_XBAR});
     } else if (!Vr.wait.npeer) {
       X.wait_nbr(st);  // fused_halo = 2: the wait is a separate one-thread kernel
     }
-    if (check) launch_row<UNIT, DICT, true>(st, lp, te, Vr, j);
-    else launch_row<UNIT, DICT, false>(st, lp, te, Vr, j);
+    if (check) launch_row<UNIT, DICT, true>(st, lp, te, em, Vr, j);
+    else launch_row<UNIT, DICT, false>(st, lp, te, em, Vr, j);
     if (!Vr.push.n) {
       if (check) X.halo(st, {A_Y, A_YT});
       else X.halo(st, {A_Y});
@@ -1477,11 +1579,14 @@ void enqueue_chunk(int chunk, cudaStream_t st, const teccl_lp* lp, const TeOp* t
   }
   if (Vr.push.n) X.wait_nbr(st);  // yt ghosts for kkt_col
   if (te) {
-    kkt_row_kernel<UNIT, true><<<Vr.nb_row, kThreads, 0, st>>>(lp->m, SellView{}, *te, Vr);
-    kkt_col_kernel<UNIT, true><<<Vc.nb_col, kThreads, 0, st>>>(lp->n, SellView{}, *te, Vc);
+    kkt_row_kernel<UNIT, 1><<<Vr.nb_row, kThreads, 0, st>>>(lp->m, SellView{}, *te, EmOp{}, Vr);
+    kkt_col_kernel<UNIT, 1><<<Vc.nb_col, kThreads, 0, st>>>(lp->n, SellView{}, *te, EmOp{}, Vc);
+  } else if (em) {
+    kkt_row_kernel<UNIT, 2><<<Vr.nb_row, kThreads, 0, st>>>(lp->m, SellView{}, TeOp{}, *em, Vr);
+    kkt_col_kernel<UNIT, 2><<<Vc.nb_col, kThreads, 0, st>>>(lp->n, SellView{}, TeOp{}, *em, Vc);
   } else {
-    kkt_row_kernel<UNIT, false><<<Vr.nb_row, kThreads, 0, st>>>(lp->m, row_view(lp), TeOp{}, Vr);
-    kkt_col_kernel<UNIT, false><<<Vc.nb_col, kThreads, 0, st>>>(lp->n, col_view(lp), TeOp{}, Vc);
+    kkt_row_kernel<UNIT, 0><<<Vr.nb_row, kThreads, 0, st>>>(lp->m, row_view(lp), TeOp{}, EmOp{}, Vr);
+    kkt_col_kernel<UNIT, 0><<<Vc.nb_col, kThreads, 0, st>>>(lp->n, col_view(lp), TeOp{}, EmOp{}, Vc);
   }
   reduce_publish_kernel<<<1, 1024, 0, st>>>(Vc, X.active() ? X.ds->sig_all : Signal{},
                                             X.active() ? X.ds->d_peer_slots : nullptr);
@@ -1527,7 +1632,7 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
     ws->st = st;
     Workspace& W = *ws;
     W.pstride = std::max<int64_t>(std::max(nb_row, nb_col), kGrid);
-    if (lp->te) {
+    if (lp->te && ((TeHold*)lp->te)->kind == 0) {
       const TeOp& t = ((TeHold*)lp->te)->op;
       W.pstride = std::max<int64_t>(W.pstride, std::max((t.n_ctask + 7) / 8, (t.n_rtask + 7) / 8));
     }
@@ -1599,12 +1704,20 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
   // working set is L2-resident (latency-bound, profiles/r01_h), mode 4 above
   // that (HBM-bound: no index stream, fastest pair measured on 4-, 8- and
   // 16-chassis LPs, profiles/r01_j_hbm_roofline.md).
-  const TeOp* te_all = (lp->te && lp->part_world == 1) ? &((TeHold*)lp->te)->op : nullptr;
-  int mf = te_all ? o->matrix_free : 0;
-  if (mf == 1) mf = (lp->n >= kAutoMatrixFreeCols && te_all->K >= 16) ? 4 : 0;
-  const TeOp* te = mf ? te_all : nullptr;
-  const bool seg_col = mf == 3, seg_row = mf == 3 || mf == 4;
-  if (!te) {
+  const TeHold* hold = (const TeHold*)lp->te;
+  const TeOp* te_all = (hold && hold->kind == 0) ? &hold->op : nullptr;
+  // epoch-block LPs (row-partitioned solves) have one matrix-free operator
+  // (per entry, both sides), selected by modes 2-4; auto keeps the stored
+  // SELL blocks there: epoch-major gathers are scattered across each epoch's
+  // families and the matrix-free block kernels measured slower
+  // (8-chassis LP on 2 GPUs: 0.716 vs 0.578 ms / iteration, profiles/r01_k)
+  const EmOp* em_all = (hold && hold->kind == 1) ? &hold->em : nullptr;
+  int mf = (te_all || em_all) ? o->matrix_free : 0;
+  if (mf == 1) mf = (te_all && lp->n >= kAutoMatrixFreeCols && te_all->K >= 16) ? 4 : 0;
+  const TeOp* te = (mf && te_all) ? te_all : nullptr;
+  const EmOp* em = (mf && em_all) ? em_all : nullptr;
+  const bool seg_col = te && mf == 3, seg_row = te && (mf == 3 || mf == 4);
+  if (!te && !em) {
     int rc = teccl_build_sell(lp, st);
     if (rc) return rc;
   }
@@ -1770,13 +1883,13 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
     TECCL_CUDA(cudaEventCreate(&b));
     TECCL_CUDA(cudaEventCreate(&c2));
     for (int w = 0; w < 3; ++w) {
-      launch_col<UNIT, DICT, false>(st, lp, te, Vc, 0);
-      launch_row<UNIT, DICT, false>(st, lp, te, Vr, 0);
+      launch_col<UNIT, DICT, false>(st, lp, te, em, Vc, 0);
+      launch_row<UNIT, DICT, false>(st, lp, te, em, Vr, 0);
     }
     TECCL_CUDA(cudaEventRecord(a, st));
-    for (int r = 0; r < sb->reps; ++r) launch_col<UNIT, DICT, false>(st, lp, te, Vc, 0);
+    for (int r = 0; r < sb->reps; ++r) launch_col<UNIT, DICT, false>(st, lp, te, em, Vc, 0);
     TECCL_CUDA(cudaEventRecord(b, st));
-    for (int r = 0; r < sb->reps; ++r) launch_row<UNIT, DICT, false>(st, lp, te, Vr, 0);
+    for (int r = 0; r < sb->reps; ++r) launch_row<UNIT, DICT, false>(st, lp, te, em, Vr, 0);
     TECCL_CUDA(cudaEventRecord(c2, st));
     TECCL_CHECK_LAUNCH();
     TECCL_CUDA(cudaEventSynchronize(c2));
@@ -1788,9 +1901,9 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
     // algorithmic bytes: SELL slice headers and every
     // stored entry once, the gathered vector once, dense operands once
     sb->matrix_free = mf;
-    if (te) {  // no stored matrix: dense vectors, the gathered operand once, capacities
+    if (te || em) {  // no stored matrix: dense vectors, the gathered operand once, capacities
       sb->bytes_col = 8.0 * nrw + 32.0 * n;
-      sb->bytes_row = 8.0 * ncw + 24.0 * m + 8.0 * (double)te->EK;
+      sb->bytes_row = 8.0 * ncw + 24.0 * m + 8.0 * (te ? (double)te->EK : (double)em->E * em->nk);
       cudaEventDestroy(a); cudaEventDestroy(b); cudaEventDestroy(c2);
       return TECCL_OK;
     }
@@ -1806,7 +1919,7 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
   }
 
   // --- chunk graph (captured once per LP and chunk length)
-  const int graph_key = chunk * 256 + (o->col_pipeline ? 1 : 0) + (te ? 2 : 0) + (o->pdl ? 4 : 0) + 8 * V.seg + 32 * o->fused_halo;
+  const int graph_key = chunk * 256 + (o->col_pipeline ? 1 : 0) + (te || em ? 2 : 0) + (o->pdl ? 4 : 0) + 8 * V.seg + 32 * o->fused_halo;
   if (o->use_graphs && W.gexec && W.graph_chunk != graph_key) {
     cudaGraphExecDestroy(W.gexec);
     W.gexec = nullptr;
@@ -1820,7 +1933,7 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
     cudaStream_t cap;
     TECCL_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
     TECCL_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
-    enqueue_chunk<UNIT, DICT>(chunk, cap, lp, te, Vc, Vr, X, y_w, yt_w);
+    enqueue_chunk<UNIT, DICT>(chunk, cap, lp, te, em, Vc, Vr, X, y_w, yt_w);
     TECCL_CUDA(cudaStreamEndCapture(cap, &g));
     TECCL_CUDA(cudaGraphInstantiate(&W.gexec, g, 0));
     TECCL_CUDA(cudaGraphDestroy(g));
@@ -1857,7 +1970,7 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
       if (gexec) {
         TECCL_CUDA(cudaGraphLaunch(gexec, st));
       } else {
-        enqueue_chunk<UNIT, DICT>(chunk, st, lp, te, Vc, Vr, X, y_w, yt_w);
+        enqueue_chunk<UNIT, DICT>(chunk, st, lp, te, em, Vc, Vr, X, y_w, yt_w);
       }
       TECCL_CHECK_LAUNCH();
       const int slot = (int)(launched % look);
@@ -2035,6 +2148,19 @@ __global__ void te_apply_kernel(TeOp op, int transpose, const double* __restrict
   }
 }
 
+__global__ void em_apply_kernel(EmOp op, int transpose, const double* __restrict__ in,
+                                double* out, double* lo, double* hi, double* c) {
+  const uint32_t count = transpose ? op.n : op.m;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x) {
+    double a, b, cc = 0.0;
+    const double v = transpose ? em_col(op, i, in, a, b, cc) : em_row(op, i, in, a, b);
+    out[i] = v;
+    lo[i] = a;
+    hi[i] = b;
+    if (transpose) c[i] = cc;
+  }
+}
+
 __global__ void seg_apply_kernel(TeOp op, int transpose, const double* __restrict__ in,
                                  double* out, double* lo, double* hi, double* c) {
   const int wi = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
@@ -2063,13 +2189,16 @@ extern "C" int teccl_lp_apply(teccl_ctx* ctx, teccl_lp* lp, int32_t transpose, i
   if (matrix_free && !lp->te) { set_error("LP has no matrix-free operator (not built by teccl_lp_build_te)"); return TECCL_EINVAL; }
   cudaStream_t st = ctx->stream;
   TECCL_CUDA(cudaSetDevice(ctx->device));
-  const int64_t nin = transpose ? lp->m : lp->n, nout = transpose ? lp->n : lp->m;
+  // inputs are gather windows (the whole vector on one device)
+  const int64_t nin = transpose ? gather_rows(lp) : gather_cols(lp), nout = transpose ? lp->n : lp->m;
   double *din = nullptr, *dout = nullptr;
   TECCL_CUDA(cudaMallocAsync((void**)&din, sizeof(double) * (nin + 1), st));
   TECCL_CUDA(cudaMallocAsync((void**)&dout, sizeof(double) * 4 * (nout + 1), st));
   TECCL_CUDA(cudaMemcpyAsync(din, in, sizeof(double) * nin, cudaMemcpyHostToDevice, st));
   double *dlo = dout + (nout + 1), *dhi = dlo + (nout + 1), *dc = dhi + (nout + 1);
-  if (matrix_free == 2) {
+  if (matrix_free && ((TeHold*)lp->te)->kind == 1) {
+    em_apply_kernel<<<grid_for(nout), kThreads, 0, st>>>(((TeHold*)lp->te)->em, transpose, din, dout, dlo, dhi, dc);
+  } else if (matrix_free == 2) {
     const TeOp& op = ((TeHold*)lp->te)->op;
     const int nt = transpose ? op.n_ctask : op.n_rtask;
     seg_apply_kernel<<<(nt + 7) / 8, kThreads, 0, st>>>(op, transpose, din, dout, dlo, dhi, dc);

@@ -736,6 +736,33 @@ int te_op_tables(const teccl_te_desc* desc, TeHold* h, cudaStream_t st) {
   return TECCL_OK;
 }
 
+// tables of the epoch-major matrix-free operator of one partition block
+int em_op_tables(const teccl_te_desc* desc, TeHold* h, cudaStream_t st) {
+  EmOp& o = h->em;
+  const int E = desc->num_edges, Nn = desc->num_nodes;
+  const int64_t K = desc->K;
+  std::vector<int4> edge4(E);
+  for (int e = 0; e < E; ++e) edge4[e] = make_int4(desc->edge_src[e], desc->edge_dst[e], desc->edge_delta[e], 0);
+  std::vector<int> cnt(Nn + 1, 0);
+  for (int e = 0; e < E; ++e) { cnt[desc->edge_src[e] + 1]++; cnt[desc->edge_dst[e] + 1]++; }
+  for (int n = 0; n < Nn; ++n) cnt[n + 1] += cnt[n];
+  std::vector<int2> incE(std::max(1, cnt[Nn]));
+  {
+    std::vector<int> fill(cnt.begin(), cnt.end() - 1);
+    for (int e = 0; e < E; ++e) {
+      incE[fill[desc->edge_src[e]]++] = make_int2(e, -1);
+      incE[fill[desc->edge_dst[e]]++] = make_int2(e, desc->edge_delta[e]);
+    }
+  }
+  std::vector<double> ninv(K);
+  for (int64_t k = 0; k < K; ++k) ninv[k] = -1.0 / (double)(k + 1);
+  int4* d4 = nullptr; int2* di = nullptr; double* dni = nullptr;
+  if (upload(edge4, &d4, st) || upload(incE, &di, st) || upload(ninv, &dni, st)) return TECCL_ECUDA;
+  for (void* p : {(void*)d4, (void*)di, (void*)dni}) h->owned.push_back(p);
+  o.edge4 = d4; o.incE = di; o.neg_inv = dni;
+  return TECCL_OK;
+}
+
 void free_te_hold(void* p) {
   TeHold* h = (TeHold*)p;
   for (void* q : h->owned) cudaFreeAsync(q, h->st);
@@ -932,7 +959,29 @@ extern "C" int teccl_lp_build_te_part(teccl_ctx* ctx, const teccl_te_desc* desc,
   TECCL_CUDA(cudaFreeAsync(row_len, st));
   TECCL_CUDA(cudaFreeAsync(col_len, st));
   TECCL_CUDA(cudaFreeAsync(mm, st));
-  for (void* p : owned) TECCL_CUDA(cudaFreeAsync(p, st));
+  // keep the tables: the PDLP kernels apply the block's rows / columns from
+  // them (epoch-major matrix-free operator, te_gen.cuh EmOp)
+  {
+    TeHold* h = new TeHold();
+    h->kind = 1;
+    EmOp& o = h->em;
+    o.d = d;
+    o.K = (uint32_t)K; o.S = (uint32_t)d.S; o.E = (uint32_t)d.E; o.G = (uint32_t)d.G;
+    o.Nn = (uint32_t)d.Nn; o.P = (uint32_t)d.P;
+    o.CW = (uint32_t)z.CW; o.RW = (uint32_t)z.RW;
+    o.SE = (uint32_t)((int64_t)d.S * d.E); o.SEG = (uint32_t)((int64_t)d.S * d.E + (int64_t)d.S * d.G);
+    o.k0 = (uint32_t)k0; o.nk = (uint32_t)(k1 - k0); o.tail_k = (uint32_t)(K - k0);
+    o.c0 = c0; o.r0 = r0; o.wc0 = cw0; o.wr0 = rw0;
+    o.n = (uint32_t)nc; o.m = (uint32_t)nr;
+    o.has_bcap = d.has_bcap; o.phase1 = d.phase1;
+    o.fCW.init(o.CW); o.fRW.init(o.RW); o.fE.init(o.E > 0 ? o.E : 1); o.fG.init(o.G > 0 ? o.G : 1);
+    o.fNn.init(o.Nn); o.fGm1.init(o.G > 1 ? o.G - 1 : 1);
+    h->owned.swap(owned);
+    h->st = st;
+    if (int rc = em_op_tables(desc, h, st)) { free_te_hold(h); return rc; }
+    lp->te = h;
+    lp->te_free = free_te_hold;
+  }
   TECCL_CUDA(cudaStreamSynchronize(st));
   const int64_t vals[16] = {c0, c1, r0, r1, cw0, cw1, rw0, rw1, k0, k1, z.n_cols, z.n_rows,
                             dmax, nnz_r, nnz_c, z.CW};

@@ -106,12 +106,212 @@ struct TeOp {
   const double* neg_inv;   // [K] -1/(k+1), the Rc costs (lp.py:133-135)
 };
 
-// Owner of the device tables behind a TeOp (lp->te).
+// Matrix-free view of one rank's block of a row-partitioned LP in the
+// epoch-major numbering (te_build.cu EmShape): columns k*CW + [F(s,e) s*E+e |
+// B(s,g) SE + s*G+g | Rd/Rc(p) SEG + 2p + rc], then the final buffers
+// B(s,g,K) at K*CW + s*G + g; rows S init rows, then k-blocks of RW =
+// [cap(e) | cons(s,n) E + s*Nn + n | cum(p) | bcap(g)], then last(s,n) and
+// bcap(g,K). The rank owns epochs [k0, k1) (+ init rows on rank 0, + the
+// tails on the last rank); gathers index the window arrays (global - w0).
+struct EmOp {
+  TeDev d;
+  FastDiv fCW, fRW, fE, fG, fNn, fGm1;
+  uint32_t K, S, E, G, Nn, P, CW, RW, SE, SEG, k0, nk, tail_k;  // owned epochs [k0, k0+nk); tail_k = K - k0
+  int64_t c0, r0, wc0, wr0;       // owned / window starts (global ids)
+  uint32_t n, m;                  // owned columns / rows
+  int has_bcap, phase1;
+  const int4* edge4;              // {src, dst, delta, 0}
+  const int2* incE;               // incident entries of node n (inc_ptr order): {e, delta} arriving, {e, -1} leaving
+  const double* neg_inv;          // [K] -1/(k+1)
+};
+
+// Owner of the device tables behind a TeOp / EmOp (lp->te).
 struct TeHold {
   TeOp op;
+  EmOp em;
+  int kind = 0;  // 0: TeOp (single device, reference numbering), 1: EmOp (partition block)
   std::vector<void*> owned;
   cudaStream_t st = nullptr;
 };
+
+__device__ __forceinline__ int64_t em_row_cons(const EmOp& o, uint32_t s, uint32_t n, int64_t k) {
+  return (int64_t)o.S + k * o.RW + o.E + (int64_t)s * o.Nn + n;
+}
+__device__ __forceinline__ int64_t em_row_last(const EmOp& o, uint32_t s, int n) {
+  const int g = __ldg(o.d.gpu_of + n), gs = __ldg(o.d.gpu_of + __ldg(o.d.snode + s));
+  return (int64_t)o.S + (int64_t)o.K * o.RW + (int64_t)s * (o.G - 1) + (g < gs ? g : g - 1);
+}
+__device__ __forceinline__ int64_t em_col_F(const EmOp& o, uint32_t s, uint32_t e, int64_t k) {
+  return k * o.CW + (int64_t)s * o.E + e;
+}
+__device__ __forceinline__ int64_t em_col_B(const EmOp& o, uint32_t s, uint32_t g, int64_t k) {
+  return k < (int64_t)o.K ? k * o.CW + o.SE + (int64_t)s * o.G + g
+                          : (int64_t)o.K * o.CW + (int64_t)s * o.G + g;
+}
+__device__ __forceinline__ int64_t em_col_Rd(const EmOp& o, uint32_t p, int64_t k) {
+  return k * o.CW + o.SEG + 2LL * p;
+}
+
+// (A^T y)_c for owned column jl of the block, with bounds and cost: the same
+// entries as te_col / gen_col, indexed in the epoch-major window.
+__device__ __forceinline__ double em_col(const EmOp& o, uint32_t jl, const double* __restrict__ yw,
+                                         double& lb, double& ub, double& c) {
+  const uint32_t K = o.K;
+  lb = 0.0; ub = INFINITY; c = 0.0;
+  const double* y = yw - o.wr0;  // y[global row]
+  const uint32_t kr = o.fCW.div(jl);
+  const int64_t k = (int64_t)o.k0 + kr;
+  if (kr >= o.tail_k) {                            // B(s,g,K)
+    const uint32_t q = jl - o.tail_k * o.CW;
+    const uint32_t s = o.fG.div(q), g = q - s * o.G;
+    const int nd = __ldg(o.d.node_of_gpu + g);
+    double a = -__ldg(y + em_row_cons(o, s, nd, K - 1));
+    if (o.has_bcap) a += __ldg(y + (int64_t)o.S + (int64_t)K * o.RW + (int64_t)o.S * (o.G - 1) + g);
+    return a;
+  }
+  const uint32_t q = jl - kr * o.CW;
+  const int64_t rk = (int64_t)o.S + k * o.RW;     // first row of epoch k
+  if (q < o.SE) {                                  // F(s,e,k)
+    const uint32_t s = o.fE.div(q), e = q - s * o.E;
+    const int4 ed = __ldg(o.edge4 + e);
+    const int sn = __ldg(o.d.snode + s);
+    const int64_t t = k + ed.z;
+    const double v_cap = __ldg(y + rk + e);
+    const double v_ini = (k == 0 && ed.x == sn) ? __ldg(y + s) : 0.0;
+    const double v_out = (k >= 1) ? __ldg(y + rk - o.RW + o.E + (int64_t)s * o.Nn + ed.x) : 0.0;
+    const double v_in = (t <= K - 1) ? __ldg(y + em_row_cons(o, s, ed.y, t)) : 0.0;
+    const bool wl = __ldg(o.d.gpu_of + ed.y) >= 0 && ed.y != sn;
+    const double v_last = (t == K - 1 && wl) ? __ldg(y + em_row_last(o, s, ed.y)) : 0.0;
+    if (k == 0 && ed.x != sn) ub = 0.0;            // lp.py:51-52
+    return v_cap + v_ini - v_out + v_in + v_last;
+  }
+  if (q < o.SEG) {                                 // B(s,g,k), k < K
+    const uint32_t q2 = q - o.SE;
+    const uint32_t s = o.fG.div(q2), g = q2 - s * o.G;
+    const int nd = __ldg(o.d.node_of_gpu + g), sn = __ldg(o.d.snode + s);
+    const int64_t rc = rk + o.E + (int64_t)s * o.Nn + nd;  // cons(s,nd,k)
+    const double v_ini = (k == 0 && nd == sn) ? __ldg(y + s) : 0.0;
+    const double v_prev = (k >= 1) ? __ldg(y + rc - o.RW) : 0.0;
+    const double v_cur = __ldg(y + rc);
+    const double v_bc = o.has_bcap ? __ldg(y + rk + o.E + (int64_t)o.S * o.Nn + o.P + g) : 0.0;
+    if (k == 0 && nd != sn) ub = 0.0;              // lp.py:57-59
+    return v_ini - v_prev + v_cur + v_bc;
+  }
+  const uint32_t q3 = q - o.SEG, p = q3 >> 1;      // Rd / Rc(p,k)
+  const int64_t cum = rk + o.E + (int64_t)o.S * o.Nn + p;
+  const double u = __ldg(o.d.pair_u + p);
+  ub = u;
+  if (!(q3 & 1)) {                                 // Rd
+    const int s = __ldg(o.d.pair_src + p), w = __ldg(o.d.pair_dst + p);
+    const double v_last = (k == K - 1) ? __ldg(y + em_row_last(o, s, w)) : 0.0;
+    return -__ldg(y + em_row_cons(o, s, w, k)) - __ldg(y + cum) - v_last;
+  }
+  const double v_next = (k + 1 <= K - 1) ? __ldg(y + cum + o.RW) : 0.0;   // Rc
+  if (o.phase1) {
+    c = (k == K - 1) ? -1.0 : 0.0;
+  } else {
+    if (k == K - 1) lb = u;                        // lp.py:64-65
+    c = __ldg(o.neg_inv + k);                      // -1/(k+1), lp.py:133-135
+  }
+  return __ldg(y + cum) - v_next;
+}
+
+// (A x)_r for owned row il of the block, with bounds (te_row / gen_row).
+__device__ __forceinline__ double em_row(const EmOp& o, uint32_t il, const double* __restrict__ xw,
+                                         double& lo, double& hi) {
+  const uint32_t K = o.K;
+  lo = 0.0; hi = 0.0;
+  const double* x = xw - o.wc0;  // x[global column]
+  const int64_t rg = o.r0 + il;
+  double a = 0.0;
+  if (rg < (int64_t)o.S) {                         // init(s)
+    const uint32_t s = (uint32_t)rg;
+    const int nd = __ldg(o.d.snode + s);
+    for (int j = __ldg(o.d.out_ptr + nd); j < __ldg(o.d.out_ptr + nd + 1); ++j)
+      a += __ldg(x + em_col_F(o, s, (uint32_t)__ldg(o.d.out_e + j), 0));
+    a += __ldg(x + em_col_B(o, s, (uint32_t)__ldg(o.d.gpu_of + nd), 0));
+    lo = hi = __ldg(o.d.out_units + s);
+    return a;
+  }
+  const uint32_t q = (uint32_t)(rg - o.S);
+  const uint32_t k = o.fRW.div(q);
+  if (k >= K) {                                    // tails
+    const uint32_t q2 = q - K * o.RW;
+    if (q2 < o.S * (o.G - 1)) {                    // last(s,n)
+      const uint32_t s = o.fGm1.div(q2), i = q2 - s * (o.G - 1);
+      const int gs = __ldg(o.d.gpu_of + __ldg(o.d.snode + s));
+      const int n = __ldg(o.d.node_of_gpu + ((int)i < gs ? i : i + 1));
+      for (int j = __ldg(o.d.inc_ptr + n); j < __ldg(o.d.inc_ptr + n + 1); ++j) {
+        const int2 t = __ldg(o.incE + j);
+        const int kk = (int)K - 1 - t.y;
+        if (t.y >= 0 && kk >= 0) a += __ldg(x + em_col_F(o, s, t.x, kk));
+      }
+      const int pr = __ldg(o.d.pair_of + s * o.Nn + n);
+      if (pr >= 0) a -= __ldg(x + em_col_Rd(o, pr, K - 1));
+      return a;
+    }
+    const uint32_t g = q2 - o.S * (o.G - 1);       // bcap(g,K)
+    for (uint32_t s = 0; s < o.S; ++s) a += __ldg(x + em_col_B(o, s, g, K));
+    lo = -INFINITY;
+    hi = o.d.blimit;
+    return a;
+  }
+  const uint32_t r = q - k * o.RW;
+  const int64_t ck = (int64_t)k * o.CW;            // first column of epoch k
+  if (r < o.E) {                                   // cap(e,k): sum_s F(s,e,k)
+    for (uint32_t s0 = 0; s0 < o.S; s0 += 8) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = (s0 + u < o.S) ? __ldg(x + ck + (int64_t)(s0 + u) * o.E + r) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) a += v[u];
+    }
+    lo = -INFINITY;
+    hi = __ldg(o.d.ecap + (int64_t)r * K + k);
+    return a;
+  }
+  if (r < o.E + o.S * o.Nn) {                      // cons(s,n,k)
+    const uint32_t r2 = r - o.E;
+    const uint32_t s = o.fNn.div(r2), n = r2 - s * o.Nn;
+    const int64_t fs = ck + (int64_t)s * o.E;      // F(s,0,k)
+    const int j0 = __ldg(o.d.inc_ptr + n), j1 = __ldg(o.d.inc_ptr + n + 1);
+    for (int jb = j0; jb < j1; jb += 8) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        v[u] = 0.0;
+        if (jb + u < j1) {
+          const int2 t = __ldg(o.incE + jb + u);
+          const int kk = (int)k - t.y;             // arriving: k - delta; leaving: k + 1
+          if (kk >= 0 && kk <= (int)K - 1) {
+            const double xv = __ldg(x + fs + (int64_t)(kk - (int)k) * o.CW + t.x);
+            v[u] = t.y < 0 ? -xv : xv;
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) a += v[u];
+    }
+    const int g = __ldg(o.d.gpu_of + n);
+    if (g >= 0) {
+      a += __ldg(x + em_col_B(o, s, g, k)) - __ldg(x + em_col_B(o, s, g, k + 1));
+      const int pr = __ldg(o.d.pair_of + s * o.Nn + n);
+      if (pr >= 0) a -= __ldg(x + em_col_Rd(o, pr, k));
+    }
+    return a;
+  }
+  if (r < o.E + o.S * o.Nn + o.P) {                // cum(p,k)
+    const uint32_t p = r - o.E - o.S * o.Nn;
+    const int64_t rd = em_col_Rd(o, p, k);
+    const double v_prev = (k >= 1) ? __ldg(x + rd - o.CW + 1) : 0.0;
+    return __ldg(x + rd + 1) - __ldg(x + rd) - v_prev;
+  }
+  const uint32_t g = r - o.E - o.S * o.Nn - o.P;  // bcap(g,k)
+  for (uint32_t s = 0; s < o.S; ++s) a += __ldg(x + em_col_B(o, s, g, k));
+  lo = -INFINITY;
+  hi = o.d.blimit;
+  return a;
+}
 
 inline void te_op_init(TeOp& o, const TeDev& d) {
   o.d = d;

@@ -18,7 +18,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _native as nat
-from .lp import LpPlan, make_plan
+from .lp import LpPlan, apply_operator, make_plan, step_bench
 
 INFO_KEYS = ("own_c0", "own_c1", "own_r0", "own_r1", "win_c0", "win_c1", "win_r0", "win_r1",
              "k0", "k1", "total_cols", "total_rows", "delta_max", "nnz_csr", "nnz_csc",
@@ -33,6 +33,19 @@ class PartLP:
     world: int
     rank: int
     info: dict
+
+    def apply(self, v: np.ndarray, transpose: bool = False, matrix_free: int = 1) -> dict:
+        """This block's rows of A.v (v over the column window) or columns of
+        A^T.v (v over the row window), stored (0) or matrix-free (1) operator."""
+        i = self.info
+        nin = (i["win_r1"] - i["win_r0"]) if transpose else (i["win_c1"] - i["win_c0"])
+        nout = (i["own_c1"] - i["own_c0"]) if transpose else (i["own_r1"] - i["own_r0"])
+        return apply_operator(self.ctx, self.handle, v, nin, nout, transpose, matrix_free)
+
+    def step_bench(self, reps: int = 50, pdlp: dict | None = None) -> dict:
+        """Half-step kernel timing on this block (world = 1 blocks only: the
+        kernels of a connected block wait for their neighbours)."""
+        return step_bench(self.ctx, self.handle, reps, pdlp)
 
     def close(self):
         if self.handle:

@@ -245,35 +245,12 @@ class DeviceLP:
         sees: matrix_free = 0 stored CSR/CSC, 1 per-entry matrix-free
         operator, 2 segment walkers (the PDLP kernels' operator)."""
         nin, nout = (self.num_rows, self.num_vars) if transpose else (self.num_vars, self.num_rows)
-        v = np.ascontiguousarray(v, dtype=np.float64)
-        if v.shape != (nin,):
-            raise ValueError(f"expected a vector of length {nin}")
-        out = {k: np.empty(nout, np.float64) for k in ("y", "lo", "hi")}
-        out["cost"] = np.empty(nout if transpose else 1, np.float64)
-        nat.check(self.ctx.lib.teccl_lp_apply(
-            self.ctx.handle, self.handle, int(bool(transpose)), int(matrix_free),
-            nat.ptr(v, C.c_double), nat.ptr(out["y"], C.c_double), nat.ptr(out["lo"], C.c_double),
-            nat.ptr(out["hi"], C.c_double), nat.ptr(out["cost"], C.c_double)))
-        if not transpose:
-            del out["cost"]
-        return out
+        return apply_operator(self.ctx, self.handle, v, nin, nout, transpose, matrix_free)
 
     def step_bench(self, reps: int = 50, pdlp: dict | None = None) -> dict:
         """Per-launch device time and algorithmic bytes of the fused kernels;
         `pdlp` overrides teccl_pdlp_opts fields (e.g. {"matrix_free": 2})."""
-        out = (C.c_double * 6)()
-        if pdlp:
-            o = nat.PdlpOpts()
-            self.ctx.lib.teccl_pdlp_default_opts(C.byref(o))
-            for k, v in pdlp.items():
-                setattr(o, k, type(getattr(o, k))(v))
-            nat.check(self.ctx.lib.teccl_pdlp_step_bench_opts(self.ctx.handle, self.handle, C.byref(o),
-                                                              int(reps), out))
-        else:
-            nat.check(self.ctx.lib.teccl_pdlp_step_bench(self.ctx.handle, self.handle, int(reps), out))
-        return {"ms_col": out[0], "ms_row": out[1], "bytes_col": out[2], "bytes_row": out[3],
-                "dict": out[4] == 1.0, "matrix_free": int(out[4]) if out[4] >= 2.0 else 0,
-                "slice": int(out[5])}
+        return step_bench(self.ctx, self.handle, reps, pdlp)
 
     def close(self) -> None:
         if self.handle:
@@ -285,6 +262,41 @@ class DeviceLP:
             self.close()
         except Exception:
             pass
+
+
+def apply_operator(ctx, handle, v: np.ndarray, nin: int, nout: int, transpose: bool,
+                   matrix_free: int) -> dict:
+    """teccl_lp_apply: A.v / A^T.v with the bounds (and costs) of the chosen
+    operator; `v` spans the gather window (the whole vector on one device)."""
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    if v.shape != (nin,):
+        raise ValueError(f"expected a vector of length {nin}")
+    out = {k: np.empty(nout, np.float64) for k in ("y", "lo", "hi")}
+    out["cost"] = np.empty(nout if transpose else 1, np.float64)
+    nat.check(ctx.lib.teccl_lp_apply(
+        ctx.handle, handle, int(bool(transpose)), int(matrix_free),
+        nat.ptr(v, C.c_double), nat.ptr(out["y"], C.c_double), nat.ptr(out["lo"], C.c_double),
+        nat.ptr(out["hi"], C.c_double), nat.ptr(out["cost"], C.c_double)))
+    if not transpose:
+        del out["cost"]
+    return out
+
+
+def step_bench(ctx, handle, reps: int = 50, pdlp: dict | None = None) -> dict:
+    """teccl_pdlp_step_bench[_opts]: per-launch time (CUDA events) and
+    algorithmic bytes of the two half-step kernels after the real setup."""
+    out = (C.c_double * 6)()
+    if pdlp:
+        o = nat.PdlpOpts()
+        ctx.lib.teccl_pdlp_default_opts(C.byref(o))
+        for k, v in pdlp.items():
+            setattr(o, k, type(getattr(o, k))(v))
+        nat.check(ctx.lib.teccl_pdlp_step_bench_opts(ctx.handle, handle, C.byref(o), int(reps), out))
+    else:
+        nat.check(ctx.lib.teccl_pdlp_step_bench(ctx.handle, handle, int(reps), out))
+    return {"ms_col": out[0], "ms_row": out[1], "bytes_col": out[2], "bytes_row": out[3],
+            "dict": out[4] == 1.0, "matrix_free": int(out[4]) if out[4] >= 2.0 else 0,
+            "slice": int(out[5])}
 
 
 def build_lp_model(t, d, cfg: EpochConfig, opts: ModelOptions | None = None,

@@ -20,7 +20,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, out):
+def _worker(rank, world, port, out, mf):
     import torch.distributed as dist
     from paper_2305_13479_b200 import EpochConfig, epoch_duration, generate_demand
     from paper_2305_13479_b200.dist import solve_partitioned
@@ -33,7 +33,8 @@ def _worker(rank, world, port, out):
         t = dgx1()
         d = generate_demand("allgather", t, 1, 25000)
         cfg = EpochConfig(epoch_duration(t, 25000, "fastest", 1), 12, "fastest", 1, 25000)
-        res = solve_partitioned(t, d, cfg, eps_rel=1e-8, device=rank, gather=True)
+        res = solve_partitioned(t, d, cfg, eps_rel=1e-8, device=rank, gather=True,
+                                pdlp={"matrix_free": mf})
         out[rank] = (res["status"], res["objective"], res["iters"],
                      res["x"] if rank == 0 else None)
     finally:
@@ -41,7 +42,8 @@ def _worker(rank, world, port, out):
 
 
 @pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
-def test_two_gpu_partition_matches_one_gpu():
+@pytest.mark.parametrize("mf", [0, 2])  # stored SELL blocks, epoch-major matrix-free blocks
+def test_two_gpu_partition_matches_one_gpu(mf):
     import torch.multiprocessing as mp
     from paper_2305_13479_b200 import (EpochConfig, SolverOptions, build_lp_model,
                                        check_lp_schedule, epoch_duration, generate_demand,
@@ -49,7 +51,7 @@ def test_two_gpu_partition_matches_one_gpu():
     from paper_2305_13479_b200.topology import dgx1
     mgr = mp.Manager()
     out = mgr.dict()
-    mp.spawn(_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    mp.spawn(_worker, args=(2, _free_port(), out, mf), nprocs=2, join=True)
     st0, obj0, it0, x = out[0]
     st1, obj1, it1, _ = out[1]
     assert st0 == st1 == "optimal" and obj0 == obj1 and it0 == it1
