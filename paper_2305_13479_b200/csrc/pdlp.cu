@@ -667,15 +667,13 @@ __global__ void __launch_bounds__(kThreads, TECCL_TE2_MINB) col_te2_kernel(TeOp 
   __shared__ double sh[32];
   const uint32_t j = 2u * (blockIdx.x * kTile + threadIdx.x);
   const bool pair = j + 1 < op.n, any = j < op.n;
-  double xj[2] = {0.0, 0.0}, x0[2] = {0.0, 0.0}, Dj[2] = {1.0, 1.0};
-  if (pair) {
-    const double2 xv = *reinterpret_cast<const double2*>(V.x + j);
-    const float2 x0v = *reinterpret_cast<const float2*>(V.x0 + j);
-    const float2 Dv = __ldg(reinterpret_cast<const float2*>(V.D + j));
-    xj[0] = xv.x; xj[1] = xv.y; x0[0] = x0v.x; x0[1] = x0v.y; Dj[0] = Dv.x; Dj[1] = Dv.y;
-  } else if (any) {
-    xj[0] = V.x[j]; x0[0] = (double)V.x0[j]; Dj[0] = (double)V.D[j];
-  }
+  // unconditional 16/8-byte loads (x, x0, D have a pad slot [n]; threads
+  // past the end load pair 0) kept raw until the epilogue, so the thread
+  // issues its table lookups and gathers while they are in flight
+  const uint32_t jl = any ? j : 0u;
+  const double2 xv = *reinterpret_cast<const double2*>(V.x + jl);
+  const float2 x0v = *reinterpret_cast<const float2*>(V.x0 + jl);
+  const float2 Dv = __ldg(reinterpret_cast<const float2*>(V.D + jl));
   pdl_wait();
   pdl_trigger();
   const PdlpState* st = V.st;
@@ -686,6 +684,8 @@ __global__ void __launch_bounds__(kThreads, TECCL_TE2_MINB) col_te2_kernel(TeOp 
   if (pair) s[1] = te_col(op, j + 1, V.y, lb[1], ub[1], cj[1]);
   if (done) return;
   const double lam = st->lam_tab[j_in_chunk];  // chunks are at most kLamTab iterations
+  const double xj[2] = {xv.x, xv.y}, x0[2] = {(double)x0v.x, (double)x0v.y};
+  const double Dj[2] = {(double)Dv.x, (double)Dv.y};
   double dx = 0.0, dx0 = 0.0, xt[2], xb[2], xn[2];
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
@@ -906,16 +906,16 @@ __global__ void __launch_bounds__(kThreads, TECCL_SEG_MINB) row_seg_kernel(TeOp 
   const int4 tk = (wi < op.n_rtask) ? __ldg(op.rtask + wi) : make_int4(0, 0, 0, 0);
   const int cnt = seg_count(tk);
   const uint32_t first = (uint32_t)tk.z;
-  double yi[kSegPerLane], y0[kSegPerLane], Ei[kSegPerLane];
+  // unconditional loads (lanes past the task's end reload its last row),
+  // kept raw until the epilogue: the gathers issue while they are in flight
+  double yi[kSegPerLane];
+  float y0f[kSegPerLane], Ef[kSegPerLane];
 #pragma unroll
   for (int h = 0; h < kSegPerLane; ++h) {
-    const int i = lane + 32 * h;
-    yi[h] = 0.0; y0[h] = 0.0; Ei[h] = 1.0;
-    if (i < cnt) {
-      yi[h] = V.y[first + i];
-      y0[h] = (double)V.y0[first + i];
-      Ei[h] = (double)V.E[first + i];
-    }
+    const uint32_t r = first + (uint32_t)max(0, min(lane + 32 * h, cnt - 1));
+    yi[h] = V.y[r];
+    y0f[h] = V.y0[r];
+    Ef[h] = V.E[r];
   }
   pdl_wait();
   pdl_trigger();
@@ -925,6 +925,9 @@ __global__ void __launch_bounds__(kThreads, TECCL_SEG_MINB) row_seg_kernel(TeOp 
   double s[kSegPerLane], lo[kSegPerLane], hi[kSegPerLane];
   seg_rows(op, tk, lane, V.xbar, s, lo, hi);
   if (done) return;
+  double y0[kSegPerLane], Ei[kSegPerLane];
+#pragma unroll
+  for (int h = 0; h < kSegPerLane; ++h) { y0[h] = (double)y0f[h]; Ei[h] = (double)Ef[h]; }
   const double lam = st->lam_tab[j_in_chunk];  // chunks are at most kLamTab iterations
   double dy = 0.0, dy0 = 0.0;
 #pragma unroll
@@ -1637,9 +1640,10 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
       W.pstride = std::max<int64_t>(W.pstride, std::max((t.n_ctask + 7) / 8, (t.n_rtask + 7) / 8));
     }
     W.rstat = W.alloc<double>(m); W.cstat = W.alloc<double>(n);
-    W.D = W.alloc<float>(n); W.E = W.alloc<float>(m);
-    W.x0 = W.alloc<float>(n); W.y0 = W.alloc<float>(m);
-    W.x = W.alloc<double>(n);
+    // pad slot [n] / [m]: the two-column kernels load pairs unconditionally
+    W.D = W.alloc<float>(n + 1); W.E = W.alloc<float>(m + 1);
+    W.x0 = W.alloc<float>(n + 1); W.y0 = W.alloc<float>(m + 1);
+    W.x = W.alloc<double>(n + 1);
     if (!ds) {  // single device: the gather windows are the owned vectors
       W.R = W.alloc<double>(m + 1); W.C = W.alloc<double>(n + 1);
       W.xt = W.alloc<double>(n + 1); W.xbar = W.alloc<double>(n + 1);
@@ -1661,6 +1665,10 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
       set_error("device allocation failed for PDLP workspace");
       return TECCL_ENOMEM;
     }
+    // defined pad values (read, never used, by the two-column kernels)
+    TECCL_CUDA(cudaMemsetAsync(W.D + n, 0, sizeof(float), st));
+    TECCL_CUDA(cudaMemsetAsync(W.x0 + n, 0, sizeof(float), st));
+    TECCL_CUDA(cudaMemsetAsync(W.x + n, 0, sizeof(double), st));
     lp->pdlp_ws = ws;
     lp->ws_free = free_workspace;
   }
