@@ -56,6 +56,9 @@ namespace teccl {
 #ifndef TECCL_TE2_MINB
 #define TECCL_TE2_MINB 8   // same, two-column column kernel (32 registers: -8 % on the 16-chassis LP)
 #endif
+#ifndef TECCL_TE2_MINB_L2
+#define TECCL_TE2_MINB_L2 6  // same, when the gathered vector fits L2 (40 registers)
+#endif
 #ifndef TECCL_COL_MINB
 #define TECCL_COL_MINB 4   // same, pipelined column kernel (64 registers: measured best)
 #endif
@@ -67,6 +70,9 @@ constexpr int kTile = kThreads;  // rows (columns) per block of the step kernels
 // auto operator (matrix_free = 1): matrix-free kernels from this many columns
 // up (configs[1], 0.97M columns, runs L2-resident on the stored SELL kernels)
 constexpr int64_t kAutoMatrixFreeCols = 3000000;
+// gathered-vector size up to which the matrix-free column kernel assumes L2
+// hits (126 MB L2 on B200)
+constexpr double kL2GatherBytes = 128.0 * 1024 * 1024;
 
 enum Q { Q_DX = 0, Q_DX0, Q_DY, Q_DY0, Q_RP, Q_DOBJ_ROW, Q_RD, Q_POBJ, Q_DOBJ_COL };
 
@@ -662,8 +668,13 @@ __global__ void __launch_bounds__(kThreads) col_te_kernel(TeOp op, Vecs V, int j
 // dense iterates and two independent gather chains in flight per thread
 // (HBM-resident LPs are short of bytes in flight with one column per
 // thread: profiles/r01_j_hbm_roofline.md).
-template <bool CHECK>
-__global__ void __launch_bounds__(kThreads, TECCL_TE2_MINB) col_te2_kernel(TeOp op, Vecs V, int j_in_chunk) {
+// WIDE: the gathered dual vector is far larger than L2 (8m > kL2GatherBytes),
+// gathers miss to HBM and latency hiding needs occupancy: 32 registers, 8
+// blocks per SM, per-column decode. Otherwise 40 registers and one family
+// decode per column pair (te_col2). Measured both ways on the 8- (y 122 MB)
+// and 16-chassis (y 1 GB) LPs, profiles/r01_j_hbm_roofline.md.
+template <bool CHECK, bool WIDE>
+__global__ void __launch_bounds__(kThreads, WIDE ? TECCL_TE2_MINB : TECCL_TE2_MINB_L2) col_te2_kernel(TeOp op, Vecs V, int j_in_chunk) {
   __shared__ double sh[32];
   const uint32_t j = 2u * (blockIdx.x * kTile + threadIdx.x);
   const bool pair = j + 1 < op.n, any = j < op.n;
@@ -680,8 +691,14 @@ __global__ void __launch_bounds__(kThreads, TECCL_TE2_MINB) col_te2_kernel(TeOp 
   const int done = st->done;  // checked before the first store: the gathers overlap it
   const double tau = st->tau, refl = st->refl;
   double s[2] = {0.0, 0.0}, lb[2] = {0.0, 0.0}, ub[2] = {0.0, 0.0}, cj[2] = {0.0, 0.0};
-  if (any) s[0] = te_col(op, j, V.y, lb[0], ub[0], cj[0]);
-  if (pair) s[1] = te_col(op, j + 1, V.y, lb[1], ub[1], cj[1]);
+  if (WIDE) {
+    if (any) s[0] = te_col(op, j, V.y, lb[0], ub[0], cj[0]);
+    if (pair) s[1] = te_col(op, j + 1, V.y, lb[1], ub[1], cj[1]);
+  } else if (pair) {
+    te_col2(op, j, V.y, s, lb, ub, cj);
+  } else if (any) {
+    s[0] = te_col(op, j, V.y, lb[0], ub[0], cj[0]);
+  }
   if (done) return;
   const double lam = st->lam_tab[j_in_chunk];  // chunks are at most kLamTab iterations
   const double xj[2] = {xv.x, xv.y}, x0[2] = {(double)x0v.x, (double)x0v.y};
@@ -1497,8 +1514,10 @@ void launch_col(cudaStream_t st, const teccl_lp* lp, const TeOp* te, const EmOp*
     else launch_iter(pdl, col_em_kernel<CHECK, false>, g, st, *em, V, j);
   } else if (te && (V.seg & 1)) {
     launch_iter(pdl, col_seg_kernel<CHECK>, (te->n_ctask + 7) / 8, st, *te, V, j);
-  } else if (te && V.col_pipe) {  // col_pipeline selects the two-column variant
-    launch_iter(pdl, col_te2_kernel<CHECK>, (int)((te->n + 2 * kTile - 1) / (2 * kTile)), st, *te, V, j);
+  } else if (te && V.col_pipe) {  // col_pipeline selects the two-column variants
+    const int g = (int)((te->n + 2 * kTile - 1) / (2 * kTile));
+    if (8.0 * te->m > kL2GatherBytes) launch_iter(pdl, col_te2_kernel<CHECK, true>, g, st, *te, V, j);
+    else launch_iter(pdl, col_te2_kernel<CHECK, false>, g, st, *te, V, j);
   } else if (te) {
     launch_iter(pdl, col_te_kernel<CHECK>, (int)((te->n + kTile - 1) / kTile), st, *te, V, j);
   } else if (V.push.n || V.wait.npeer) {  // fused peer exchange compiled in only where used

@@ -390,6 +390,72 @@ __device__ __forceinline__ double te_col(const TeOp& o, uint32_t v, const double
   return a;
 }
 
+// (A^T y) for the adjacent columns v, v+1 (v even, v+1 < n): when both are
+// epochs k, k+1 of one flow or buffer family -- all but one pair per family
+// -- the family's table lookups and index math are done once and the
+// gathers of the two epochs are adjacent; otherwise te_col twice.
+__device__ __forceinline__ void te_col2(const TeOp& o, uint32_t v, const double* __restrict__ y,
+                                        double (&a)[2], double (&lb)[2], double (&ub)[2],
+                                        double (&c)[2]) {
+  const uint32_t K = o.K;
+  if (v + 1 < o.nF) {
+    const uint32_t s = o.fSB.div(v);
+    const uint32_t q = v - s * o.SB;
+    if (q + 1 < o.EK) {
+      const uint32_t e = o.fK.div(q), k = q - e * K;
+      if (k + 1 < K) {                             // F(s,e,k), F(s,e,k+1)
+        const int sn = __ldg(o.d.snode + s);
+        const int2* sr = o.sntab + s * o.Nn;
+        const int4 ed = __ldg(o.edge4 + e);
+        const uint32_t cu = (uint32_t)__ldg(&sr[ed.x].x) & kIdxMask;
+        const uint32_t cw = (uint32_t)__ldg(&sr[ed.y].x);
+        const uint32_t t = k + (uint32_t)ed.z;
+        const double* yc = y + o.S + q;
+        const double* yo = y + cu + k;             // cons(s,u,k-1+h) = yo[h-1]
+        const double* yi = y + (cw & kIdxMask) + t;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t kh = k + h, th = t + h;
+          const double v_cap = __ldg(yc + h);
+          const double v_ini = (kh == 0 && ed.x == sn) ? __ldg(y + s) : 0.0;
+          const double v_out = (kh >= 1) ? __ldg(yo + h - 1) : 0.0;
+          const double v_in = (th <= K - 1) ? __ldg(yi + h) : 0.0;
+          const double v_last = (th == K - 1 && (cw & kSignBit)) ? __ldg(y + (cw & kIdxMask) + K) : 0.0;
+          a[h] = v_cap + v_ini - v_out + v_in + v_last;
+          lb[h] = 0.0;
+          ub[h] = (kh == 0 && ed.x != sn) ? 0.0 : INFINITY;  // lp.py:51-52
+          c[h] = 0.0;
+        }
+        return;
+      }
+    } else if (q >= o.EK && q + 1 < o.SB) {
+      const uint32_t qb = q - o.EK;
+      const uint32_t g = o.fK1.div(qb), k = qb - g * (K + 1);
+      if (k + 1 <= K) {                            // B(s,g,k), B(s,g,k+1)
+        const int sn = __ldg(o.d.snode + s);
+        const int nd = __ldg(o.d.node_of_gpu + g);
+        const uint32_t rb = (uint32_t)__ldg(&o.sntab[s * o.Nn + nd].x) & kIdxMask;
+        const double* yr = y + rb + k;             // cons(s,nd,k+h) = yr[h]
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t kh = k + h;
+          const double v_ini = (kh == 0 && nd == sn) ? __ldg(y + s) : 0.0;
+          const double v_prev = (kh >= 1) ? __ldg(yr + h - 1) : 0.0;
+          const double v_cur = (kh <= K - 1) ? __ldg(yr + h) : 0.0;
+          const double v_bc = o.has_bcap ? __ldg(y + o.R_bcap + qb + h) : 0.0;
+          a[h] = v_ini - v_prev + v_cur + v_bc;
+          lb[h] = 0.0;
+          ub[h] = (kh == 0 && nd != sn) ? 0.0 : INFINITY;  // lp.py:57-59
+          c[h] = 0.0;
+        }
+        return;
+      }
+    }
+  }
+  a[0] = te_col(o, v, y, lb[0], ub[0], c[0]);
+  a[1] = te_col(o, v + 1, y, lb[1], ub[1], c[1]);
+}
+
 // sum over s < S of x[s*SB + off], loads issued 8 at a time
 __device__ __forceinline__ double te_sum_sources(const TeOp& o, const double* __restrict__ x, uint32_t off) {
   double a = 0.0;
@@ -496,7 +562,10 @@ __device__ __forceinline__ double te_row(const TeOp& o, uint32_t i, const double
 //   w = off | count << 24   (off = epoch offset inside the segment)
 enum SegKind { SEG_F = 0, SEG_B = 1, SEG_P = 2,                          // columns
                SEG_INIT = 3, SEG_CAP = 4, SEG_CONS = 5, SEG_CUM = 6, SEG_BCAP = 7 };  // rows
-constexpr int kSegPerLane = 2;
+#ifndef TECCL_SEG_PER_LANE
+#define TECCL_SEG_PER_LANE 2  // entries per lane of a segment task (task = 32 x this)
+#endif
+constexpr int kSegPerLane = TECCL_SEG_PER_LANE;
 constexpr int kSegTask = 32 * kSegPerLane;
 
 __device__ __forceinline__ int seg_count(const int4& t) { return (int)((uint32_t)t.w >> 24); }
