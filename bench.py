@@ -9,6 +9,12 @@ constraint matrix is already resident in HBM when the timed region starts.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 
+`roofline`: the dominant half-step kernel's algorithmic bytes per launch
+over its CUDA-event launch time, on an HBM-resident LP of the same family
+(8-chassis NDv2 AllGather, K=1800: 53M columns) where the solver runs its
+large-LP (matrix-free) kernels; `roofline_l2_resident`: the same for
+configs[1] itself, whose ~70 MB working set stays in L2 between iterations.
+
 N>1 (torchrun): every rank solves its own instance of the same LP (weak
 scaling, no data-path collective); value = max-over-ranks step time / N.
 --impl reference times the reference's CPU path (the oracle restatement of

@@ -684,6 +684,8 @@ int te_op_tables(const teccl_te_desc* desc, TeHold* h, cudaStream_t st) {
       incp[fill[desc->edge_dst[e]]++] = make_int2((int)(e * K - desc->edge_delta[e]), desc->edge_delta[e]);
     }
   }
+  o.dmax = 0;
+  for (int e = 0; e < E; ++e) o.dmax = std::max(o.dmax, (int)desc->edge_delta[e]);
   // segment tasks, in memory order (seg_cols / seg_rows in te_gen.cuh)
   std::vector<int4> ct, rt;
   auto add = [](std::vector<int4>& v, int kind, int a, int b, int64_t start, int64_t len) {

@@ -104,6 +104,7 @@ struct TeOp {
   const int4* rtask;
   int n_ctask, n_rtask;
   const double* neg_inv;   // [K] -1/(k+1), the Rc costs (lp.py:133-135)
+  int dmax;                // largest edge delay (epochs)
 };
 
 // Matrix-free view of one rank's block of a row-partitioned LP in the
@@ -326,6 +327,7 @@ inline void te_op_init(TeOp& o, const TeDev& d) {
   o.fSB.init(o.SB > 0 ? o.SB : 1); o.fCB.init(o.CB > 0 ? o.CB : 1);
   o.edge4 = nullptr; o.sntab = nullptr; o.incp = nullptr;
   o.ctask = nullptr; o.rtask = nullptr; o.n_ctask = 0; o.n_rtask = 0; o.neg_inv = nullptr;
+  o.dmax = 0;
 }
 
 // (A^T y)_v for column v, with its bounds and cost (gen_col in te_build.cu
@@ -690,7 +692,30 @@ __device__ __forceinline__ void seg_rows(const TeOp& o, const int4& t, int lane,
       last[h] = (k == (int)K);
       kk[h] = last[h] ? (int)K - 1 : k;
     }
-    for (int jb = j0; jb < j1; jb += 4) {
+    // interior task (every epoch's terms exist: k - delay >= 0, k + 1 <= K-1,
+    // no last row, all lanes busy): unpredicated gathers at fixed offsets
+    // from one base, the sign as a +-1 weight (same sums in the same order)
+    const bool interior = cnt == kSegTask && off >= o.dmax && off + kSegTask <= (int)K - 1;
+    if (interior) {
+      const double* xb = xs + off + lane;          // term (e*K + c) of epoch off + lane: xb[e*K + c]
+      for (int jb = j0; jb < j1; jb += 4) {
+        int2 e4[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) e4[u] = (jb + u < j1) ? __ldg(o.incp + jb + u) : make_int2(0, 0);
+        double w[4], v[kSegPerLane][4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          w[u] = (jb + u < j1) ? (e4[u].y < 0 ? -1.0 : 1.0) : 0.0;
+#pragma unroll
+          for (int h = 0; h < kSegPerLane; ++h) v[h][u] = __ldg(xb + e4[u].x + 32 * h);
+        }
+#pragma unroll
+        for (int h = 0; h < kSegPerLane; ++h)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) a[h] = fma(w[u], v[h][u], a[h]);
+      }
+    }
+    for (int jb = interior ? j1 : j0; jb < j1; jb += 4) {
       int2 e4[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) e4[u] = (jb + u < j1) ? __ldg(o.incp + jb + u) : make_int2(0, (int)K);
