@@ -403,6 +403,14 @@ __device__ __forceinline__ double clampd(double v, double lo, double hi) {
   return fmin(fmax(v, lo), hi);
 }
 
+// Dual step y+ = y - sE (Ax - P[lo,hi](Ax - y / (sE))) without the fp64
+// division: with w = sE Ax - y and sE > 0, sE P[lo,hi](u) = P[sE lo, sE hi](sE u),
+// so y+ = P[sE lo, sE hi](w) - w.
+__device__ __forceinline__ double dual_step(double yi, double s, double se, double lo, double hi) {
+  const double w = fma(se, s, -yi);
+  return clampd(w, se * lo, se * hi) - w;
+}
+
 template <bool DICT>
 __device__ __forceinline__ void col_data(const Bounds& B, int64_t j, double& lb, double& ub,
                                          double& c) {
@@ -600,7 +608,7 @@ __global__ void __launch_bounds__(kThreads, TECCL_ROW_MINB) row_step_kernel(int3
   double dy = 0.0, dy0 = 0.0;
   if (i < (uint32_t)m) {
     const double se = sigma * Ei;
-    const double yt = yi - se * (s - clampd(s - yi / se, lo, hi));
+    const double yt = dual_step(yi, s, se, lo, hi);
     const double yn = lam * ((1.0 + refl) * yt - refl * yi) + (1.0 - lam) * y0;
     V.y[i] = yn;
     wrote = PEER && push_entry<CHECK>(V.push, i, yn, yt);
@@ -753,7 +761,7 @@ __global__ void __launch_bounds__(kThreads) row_te_kernel(TeOp op, Vecs V, int j
   double dy = 0.0, dy0 = 0.0;
   if (i < op.m) {
     const double se = sigma * Ei;
-    const double yt = yi - se * (s - clampd(s - yi / se, lo, hi));
+    const double yt = dual_step(yi, s, se, lo, hi);
     V.y[i] = lam * ((1.0 + refl) * yt - refl * yi) + (1.0 - lam) * y0;
     if (CHECK) {
       V.yt[i] = yt;
@@ -840,7 +848,7 @@ __global__ void __launch_bounds__(kThreads) row_em_kernel(EmOp op, Vecs V, int j
   double dy = 0.0, dy0 = 0.0;
   if (i < op.m) {
     const double se = sigma * Ei;
-    const double yt = yi - se * (s - clampd(s - yi / se, lo, hi));
+    const double yt = dual_step(yi, s, se, lo, hi);
     const double yn = lam * ((1.0 + refl) * yt - refl * yi) + (1.0 - lam) * y0;
     V.y[i] = yn;
     wrote = PEER && push_entry<CHECK>(V.push, i, yn, yt);
@@ -953,7 +961,7 @@ __global__ void __launch_bounds__(kThreads, TECCL_SEG_MINB) row_seg_kernel(TeOp 
     if (i < cnt) {
       const uint32_t r = first + i;
       const double se = sigma * Ei[h];
-      const double yt = yi[h] - se * (s[h] - clampd(s[h] - yi[h] / se, lo[h], hi[h]));
+      const double yt = dual_step(yi[h], s[h], se, lo[h], hi[h]);
       V.y[r] = lam * ((1.0 + refl) * yt - refl * yi[h]) + (1.0 - lam) * y0[h];
       if (CHECK) {
         V.yt[r] = yt;
