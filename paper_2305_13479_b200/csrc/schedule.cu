@@ -164,27 +164,11 @@ extern "C" int teccl_schedule_te(const teccl_te_desc* desc, const double* x, dou
   J.G = G;
   J.SB = (int64_t)J.E * J.K + (int64_t)G * (J.K + 1);
 
-  std::vector<std::vector<Ev>> per(J.S);
-  std::vector<std::string> errs(J.S);
-  std::vector<char> ok(J.S, 1);
-  int nt = threads > 0 ? threads : (int)std::max(1u, std::thread::hardware_concurrency());
-  nt = std::max(1, std::min(nt, J.S));
-  std::vector<std::thread> pool;
-  for (int w = 0; w < nt; ++w)
-    pool.emplace_back([&, w]() {
-      for (int s = w; s < J.S; s += nt) ok[s] = run_source(J, s, per[s], errs[s]);
-    });
-  for (auto& t : pool) t.join();
-  for (int s = 0; s < J.S; ++s)
-    if (!ok[s]) { set_error(errs[s]); return TECCL_EINVAL; }
-
-  // concatenate in source order (the reference's generation order), then the
-  // stable sort by (epoch, str(source), str(src), str(dst), chunk) and merge
-  auto* L = new EventList();
-  size_t total = 0;
-  for (auto& v : per) total += v.size();
-  L->ev.reserve(total);
-  for (auto& v : per) L->ev.insert(L->ev.end(), v.begin(), v.end());
+  // key order of the reference's event list: (epoch, str(source), str(src),
+  // str(dst), chunk), stable in generation order; equal keys are merged by
+  // summing in that order. Every key carries its source, so each source's
+  // list is sorted and merged in its own thread, and the global order is a
+  // merge of the per-source lists by (epoch, source rank).
   auto key_less = [&](const Ev& a, const Ev& b) {
     if (a.epoch != b.epoch) return a.epoch < b.epoch;
     const int sa = source_rank[a.src_slot], sb = source_rank[b.src_slot];
@@ -195,20 +179,59 @@ extern "C" int teccl_schedule_te(const teccl_te_desc* desc, const double* x, dou
     if (da != db) return da < db;
     return a.chunk < b.chunk;
   };
-  std::stable_sort(L->ev.begin(), L->ev.end(), key_less);
-  std::vector<Ev> merged;
-  merged.reserve(L->ev.size());
-  for (const Ev& e : L->ev) {
-    if (!merged.empty()) {
-      Ev& m = merged.back();
-      if (m.src_slot == e.src_slot && m.chunk == e.chunk && m.edge == e.edge && m.epoch == e.epoch) {
-        m.frac += e.frac;
-        continue;
+  auto sort_merge = [&](std::vector<Ev>& v) {
+    std::stable_sort(v.begin(), v.end(), key_less);
+    size_t w = 0;
+    for (size_t i = 0; i < v.size(); ++i) {
+      if (w > 0) {
+        Ev& m = v[w - 1];
+        const Ev& e = v[i];
+        if (m.src_slot == e.src_slot && m.chunk == e.chunk && m.edge == e.edge && m.epoch == e.epoch) {
+          m.frac += e.frac;
+          continue;
+        }
       }
+      v[w++] = v[i];
     }
-    merged.push_back(e);
+    v.resize(w);
+  };
+  std::vector<std::vector<Ev>> per(J.S);
+  std::vector<std::string> errs(J.S);
+  std::vector<char> ok(J.S, 1);
+  int nt = threads > 0 ? threads : (int)std::max(1u, std::thread::hardware_concurrency());
+  nt = std::max(1, std::min(nt, J.S));
+  std::vector<std::thread> pool;
+  for (int w = 0; w < nt; ++w)
+    pool.emplace_back([&, w]() {
+      for (int s = w; s < J.S; s += nt) {
+        ok[s] = run_source(J, s, per[s], errs[s]);
+        if (ok[s]) sort_merge(per[s]);
+      }
+    });
+  for (auto& t : pool) t.join();
+  for (int s = 0; s < J.S; ++s)
+    if (!ok[s]) { set_error(errs[s]); return TECCL_EINVAL; }
+
+  auto* L = new EventList();
+  size_t total = 0;
+  for (auto& v : per) total += v.size();
+  L->ev.reserve(total);
+  std::vector<int> by_rank(J.S);
+  for (int s = 0; s < J.S; ++s) by_rank[s] = s;
+  std::stable_sort(by_rank.begin(), by_rank.end(),
+                   [&](int a, int b) { return source_rank[a] < source_rank[b]; });
+  std::vector<size_t> pos(J.S, 0);
+  for (int k = 0; k < J.K; ++k)
+    for (int s : by_rank) {
+      const std::vector<Ev>& v = per[s];
+      size_t& i = pos[s];
+      while (i < v.size() && v[i].epoch == k) L->ev.push_back(v[i++]);
+    }
+  if (L->ev.size() != total) {
+    delete L;
+    set_error("schedule event outside the horizon");
+    return TECCL_EINVAL;
   }
-  L->ev.swap(merged);
   *out = L;
   *n_events = (int64_t)L->ev.size();
   return TECCL_OK;

@@ -17,7 +17,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .errors import ConservationError, ValidationError
+from .errors import ConservationError, SolverBackendError, ValidationError
 from .lp import TOL, LpPlan
 
 
@@ -66,14 +66,46 @@ def lp_rates_to_schedule(sol, t=None, d=None, cfg=None) -> Schedule:
     if not sol.feasible:
         raise ValidationError(f"cannot schedule a solution with status {sol.status}")
     plan: LpPlan = sol.model.plan
-    x = np.asarray(sol.x, dtype=np.float64)
+    meta = {}
+    try:
+        events = _decompose_solution(plan, sol.x)
+    except ConservationError:
+        # A loose first-order solution (e.g. eps_rel 1e-4) can leave a chunk
+        # short by ~eps after the flow repair. Polish it on the device --
+        # warm-started from this solution -- to POLISH_EPS and decompose that
+        # (the reference's exact HiGHS solutions never need this).
+        eps = sol.meta.get("eps_rel")
+        if eps is None or eps <= POLISH_EPS or not hasattr(sol.model, "handle"):
+            raise
+        from .solver import SolverOptions, solve
+        pol = solve(sol.model, SolverOptions(eps_rel=POLISH_EPS, device=sol.model.ctx.device,
+                                             time_limit=600.0, max_iters=50_000_000), warm=sol)
+        if not pol.feasible:
+            raise
+        meta = {"polished_from_eps": eps, "polish_eps": POLISH_EPS,
+                "polish_iters": pol.meta["iters"], "polish_device_s": pol.meta["device_seconds"]}
+        events = _decompose_solution(plan, pol.x)
+        sol = pol
+    return Schedule(tau=plan.cfg.tau, events=tuple(events),
+                    completion_epoch=lp_completion_epoch(sol), chunk_size=plan.demand.chunk_size,
+                    meta=meta)
+
+
+POLISH_EPS = 1e-8
+
+
+def _decompose_solution(plan: LpPlan, x) -> list:
+    x = np.asarray(x, dtype=np.float64)
     tol = TOL
     if max_deficit(plan, x) > EXACT:  # first-order solution: make every read traceable
         x = repair_flows(plan, x)
         tol = DUST
-    events = decompose_native(plan, x, tol)
-    return Schedule(tau=plan.cfg.tau, events=tuple(events),
-                    completion_epoch=lp_completion_epoch(sol), chunk_size=plan.demand.chunk_size)
+    try:
+        return decompose_native(plan, x, tol)
+    except SolverBackendError as exc:  # the native decomposition reports residues as errors
+        if "conservation residue" in str(exc) or "did not converge" in str(exc):
+            raise ConservationError(str(exc)) from exc
+        raise
 
 
 EXACT = 1e-9  # deficits below this: leave the solution untouched (vertex solutions)
@@ -228,9 +260,16 @@ def decompose_native(plan: LpPlan, x: np.ndarray, tol: float = TOL, need_tol: fl
     nat.check(lib.teccl_schedule_fetch(h, nat.ptr(ss, C.c_int32), nat.ptr(cc, C.c_int32),
                                        nat.ptr(ee, C.c_int32), nat.ptr(kk, C.c_int32),
                                        nat.ptr(ff, C.c_double)))
-    src = plan.sources
-    return [ScheduleEvent(src[int(ss[i])], int(cc[i]), nodes[int(plan.esrc[ee[i]])],
-                          nodes[int(plan.edst[ee[i]])], int(kk[i]), float(ff[i])) for i in range(n)]
+    if n == 0:
+        return []
+    node_arr = np.empty(len(nodes), dtype=object)
+    node_arr[:] = list(nodes)
+    src_arr = np.empty(len(plan.sources), dtype=object)
+    src_arr[:] = list(plan.sources)
+    e = ee[:n]
+    return list(map(ScheduleEvent, src_arr[ss[:n]].tolist(), cc[:n].tolist(),
+                    node_arr[plan.esrc[e]].tolist(), node_arr[plan.edst[e]].tolist(),
+                    kk[:n].tolist(), ff[:n].tolist()))
 
 
 def decompose(plan: LpPlan, x: np.ndarray, tol: float = TOL, need_tol: float = TOL) -> list:

@@ -116,9 +116,10 @@ def _upload_generic(m, device: int) -> DeviceLP:
 
 
 def solve(m, opts: SolverOptions | None = None, relax_integrality: bool = False,
-          verbose: int = 0) -> Solution:
+          verbose: int = 0, warm: Solution | None = None) -> Solution:
     """Solve an LP on the GPU. `m` is a DeviceLP (from build_lp_model) or any
-    reference-style Model whose variables are all continuous."""
+    reference-style Model whose variables are all continuous. `warm`: a
+    previous Solution of the same LP (x and y) to start the iteration from."""
     opts = opts or SolverOptions()
     name = _backend_name(opts)
     if name != BACKEND:
@@ -137,6 +138,12 @@ def solve(m, opts: SolverOptions | None = None, relax_integrality: bool = False,
     y = np.empty(dev_lp.num_rows)
     res = nat.PdlpResult()
     o = pdlp_options(opts, verbose)
+    if warm is not None:
+        if warm.x is None or warm.y is None or len(warm.x) != len(x) or len(warm.y) != len(y):
+            raise ValidationError("warm start needs x and y of this LP")
+        x[:] = warm.x
+        y[:] = warm.y
+        o.warm_start = 1
     nat.check(dev_lp.ctx.lib.teccl_pdlp_solve(dev_lp.ctx.handle, dev_lp.handle, C.byref(o),
                                               nat.ptr(x, C.c_double), nat.ptr(y, C.c_double),
                                               C.byref(res)))
