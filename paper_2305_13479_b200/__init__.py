@@ -15,6 +15,7 @@ from .lp import DeviceLP, LpPlan, ModelOptions, build_lp_model, lp_completion_ep
 from .schedule import Schedule, ScheduleEvent, lp_rates_to_schedule
 from .solver import Solution, SolverOptions, min_feasible_horizon, solve
 from .topology import Edge, Topology, validate_topology
+from .workflow import SynthesisResult, synthesize
 
 __all__ = [
     "CheckReport", "check_lp_schedule", "Demand", "generate_demand", "merge_demands",
@@ -23,5 +24,5 @@ __all__ = [
     "ValidationError", "DeviceLP", "LpPlan", "ModelOptions", "build_lp_model",
     "lp_completion_epoch", "make_plan", "Solution", "SolverOptions", "min_feasible_horizon",
     "solve", "Edge", "Topology", "validate_topology", "Schedule", "ScheduleEvent",
-    "lp_rates_to_schedule",
+    "lp_rates_to_schedule", "SynthesisResult", "synthesize",
 ]

@@ -62,13 +62,19 @@ def save_schedule(s: Schedule, path) -> None:
 def lp_rates_to_schedule(sol, t=None, d=None, cfg=None) -> Schedule:
     """Decompose an LP solution (from this package's solve) into fractional
     per-chunk events; raises ConservationError on residue, like the reference."""
+    return schedule_with_flows(sol)[0]
+
+
+def schedule_with_flows(sol) -> tuple:
+    """(Schedule, x): the schedule and the exactly conserving flow vector its
+    events were peeled from (the repaired / polished solution), for replay."""
     from .lp import lp_completion_epoch
     if not sol.feasible:
         raise ValidationError(f"cannot schedule a solution with status {sol.status}")
     plan: LpPlan = sol.model.plan
     meta = {}
     try:
-        events = _decompose_solution(plan, sol.x)
+        events, x = _decompose_solution(plan, sol.x)
     except ConservationError:
         # A loose first-order solution (e.g. eps_rel 1e-4) can leave a chunk
         # short by ~eps after the flow repair. Polish it on the device --
@@ -84,24 +90,24 @@ def lp_rates_to_schedule(sol, t=None, d=None, cfg=None) -> Schedule:
             raise
         meta = {"polished_from_eps": eps, "polish_eps": POLISH_EPS,
                 "polish_iters": pol.meta["iters"], "polish_device_s": pol.meta["device_seconds"]}
-        events = _decompose_solution(plan, pol.x)
+        events, x = _decompose_solution(plan, pol.x)
         sol = pol
-    return Schedule(tau=plan.cfg.tau, events=tuple(events),
-                    completion_epoch=lp_completion_epoch(sol), chunk_size=plan.demand.chunk_size,
-                    meta=meta)
+    sched = Schedule(tau=plan.cfg.tau, events=tuple(events), completion_epoch=lp_completion_epoch(sol),
+                     chunk_size=plan.demand.chunk_size, meta=meta)
+    return sched, x
 
 
 POLISH_EPS = 1e-8
 
 
-def _decompose_solution(plan: LpPlan, x) -> list:
+def _decompose_solution(plan: LpPlan, x) -> tuple:
     x = np.asarray(x, dtype=np.float64)
     tol = TOL
     if max_deficit(plan, x) > EXACT:  # first-order solution: make every read traceable
         x = repair_flows(plan, x)
         tol = DUST
     try:
-        return decompose_native(plan, x, tol)
+        return decompose_native(plan, x, tol), x
     except SolverBackendError as exc:  # the native decomposition reports residues as errors
         if "conservation residue" in str(exc) or "did not converge" in str(exc):
             raise ConservationError(str(exc)) from exc
