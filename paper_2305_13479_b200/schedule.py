@@ -106,6 +106,10 @@ def _decompose_solution(plan: LpPlan, x) -> tuple:
     if max_deficit(plan, x) > EXACT:  # first-order solution: make every read traceable
         x = repair_flows(plan, x)
         tol = DUST
+        # reads only shrink in the repair: a pair whose reads no longer add up
+        # to its demand would end in a residue -- say so before peeling
+        if plan.P and float((plan.pair_units - plan.rd_matrix(x).sum(axis=1)).max()) > TOL:
+            raise ConservationError("repaired flows deliver less than the demand")
     try:
         return decompose_native(plan, x, tol), x
     except SolverBackendError as exc:  # the native decomposition reports residues as errors
