@@ -270,16 +270,34 @@ __global__ void wait_kernel(Wait Wt, PdlpState* st) {
 // of every rank's slot table (own + peers), then signal all peers.
 __global__ void __launch_bounds__(1024) reduce_publish_kernel(Vecs V, Signal S,
                                                               double* const* peer_slots) {
-  __shared__ double sh[32];
+  __shared__ double wsum[kNQ][32];
   __shared__ double q[kNQ];
   if (V.st->done) return;
+  // all nine quantities in one pass (every thread's loads in flight
+  // together), then one warp-shuffle + shared-memory reduction
+  double a[kNQ];
+#pragma unroll
+  for (int k = 0; k < kNQ; ++k) a[k] = 0.0;
+  const int nbmax = max(V.nb_row, V.nb_col);
+  for (int b = threadIdx.x; b < nbmax; b += blockDim.x) {
+#pragma unroll
+    for (int k = 0; k < kNQ; ++k) {
+      const bool row_q = (k == Q_DY || k == Q_DY0 || k == Q_RP || k == Q_DOBJ_ROW);
+      if (b < (row_q ? V.nb_row : V.nb_col)) a[k] += V.part[k * V.pstride + b];
+    }
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+#pragma unroll
   for (int k = 0; k < kNQ; ++k) {
-    const bool row_q = (k == Q_DY || k == Q_DY0 || k == Q_RP || k == Q_DOBJ_ROW);
-    const int nb = row_q ? V.nb_row : V.nb_col;
-    double a = 0.0;
-    for (int b = threadIdx.x; b < nb; b += blockDim.x) a += V.part[k * V.pstride + b];
-    a = block_sum(a, sh);
-    if (threadIdx.x == 0) q[k] = a;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a[k] += __shfl_xor_sync(0xffffffffu, a[k], o);
+    if (l == 0) wsum[k][w] = a[k];
+  }
+  __syncthreads();
+  if (threadIdx.x < kNQ) {
+    double t = 0.0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += wsum[threadIdx.x][i];
+    q[threadIdx.x] = t;
   }
   __syncthreads();
   if (threadIdx.x < kNQ) {
