@@ -100,6 +100,22 @@ int teccl_lp_build_te_part(teccl_ctx* ctx, const teccl_te_desc* desc, int32_t wo
 int teccl_dist_export(teccl_ctx* ctx, teccl_lp* lp, uint8_t* blob, int64_t* blob_len);
 int teccl_dist_connect(teccl_ctx* ctx, teccl_lp* lp, const uint8_t* blobs, int64_t blob_len);
 
+/* Source-partitioned solve of a WHOLE LP from teccl_lp_build_te (every rank
+ * holds it; setup is the single-device one, redundant on every rank). Rank
+ * `rank` of `world` updates the columns of sources [s0, s1) and of their
+ * pairs and the init / conservation / cumulative rows of those; the capacity
+ * (and buffer-limit) rows couple the sources: every iteration each rank
+ * stores its partial row sums into every rank's buffer over peer memory and
+ * all ranks take those rows' dual step identically. No reference
+ * counterpart (new). info8 = {s0, s1, p0, p1, c0, c1, q0, q1}: own sources,
+ * pairs, flow+buffer columns [c0, c1) and Rd/Rc columns [q0, q1). Then
+ * export / all-gather / connect the blobs (rank order) as for
+ * teccl_dist_*, and call teccl_pdlp_solve; x/y come back whole, valid on
+ * this rank's columns / rows. */
+int teccl_src_setup(teccl_ctx* ctx, teccl_lp* lp, int32_t world, int32_t rank, int64_t* info8);
+int teccl_src_export(teccl_ctx* ctx, teccl_lp* lp, uint8_t* blob, int64_t* blob_len);
+int teccl_src_connect(teccl_ctx* ctx, teccl_lp* lp, const uint8_t* blobs, int64_t blob_len);
+
 /* Generic LP upload (minimise obj.x s.t. row_lo <= A x <= row_hi,
  * var_lb <= x <= var_ub; +-INFINITY allowed). Replaces the matrix assembly of
  * collsched.solver.solve (solver.py:96-118) for any Model the reference

@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 EXPORTED = (
     "teccl_last_error", "teccl_version", "teccl_ctx_create", "teccl_ctx_destroy",
     "teccl_ctx_sync", "teccl_lp_build_te", "teccl_lp_build_te_part", "teccl_dist_export",
-    "teccl_dist_connect", "teccl_lp_from_csr", "teccl_lp_dims",
+    "teccl_dist_connect", "teccl_src_setup", "teccl_src_export", "teccl_src_connect", "teccl_lp_from_csr", "teccl_lp_dims",
     "teccl_lp_export", "teccl_lp_export_csc", "teccl_lp_destroy",
     "teccl_pdlp_default_opts", "teccl_pdlp_solve", "teccl_pdlp_solve_dev",
     "teccl_spmv_bench", "teccl_pdlp_step_bench", "teccl_pdlp_step_bench_opts", "teccl_lp_apply", "teccl_check_te", "teccl_check_te_dev",
@@ -109,6 +109,9 @@ def load(path: str | None = None):
                                                  _p(C.c_int64)]),
             "teccl_dist_export": (C.c_int, [vp, vp, _p(C.c_uint8), _p(C.c_int64)]),
             "teccl_dist_connect": (C.c_int, [vp, vp, _p(C.c_uint8), C.c_int64]),
+            "teccl_src_setup": (C.c_int, [vp, vp, C.c_int32, C.c_int32, _p(C.c_int64)]),
+            "teccl_src_export": (C.c_int, [vp, vp, _p(C.c_uint8), _p(C.c_int64)]),
+            "teccl_src_connect": (C.c_int, [vp, vp, _p(C.c_uint8), C.c_int64]),
             "teccl_lp_from_csr": (C.c_int, [vp, C.c_int32, C.c_int32, C.c_int64, _p(C.c_int64),
                                             _p(C.c_int32), _p(C.c_double), _p(C.c_double),
                                             _p(C.c_double), _p(C.c_double), _p(C.c_double),

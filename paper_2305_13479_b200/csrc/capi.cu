@@ -293,6 +293,7 @@ extern "C" int teccl_lp_destroy(teccl_lp* lp) {
   }
   if (lp->pdlp_ws && lp->ws_free) lp->ws_free(lp->pdlp_ws);
   if (lp->dist && lp->dist_free) lp->dist_free(lp->dist);
+  if (lp->src && lp->src_free) lp->src_free(lp->src);
   if (lp->te && lp->te_free) lp->te_free(lp->te);
   void* ptrs[] = {lp->row_ptr, lp->col, lp->val, lp->col_ptr, lp->row, lp->cval,
                   lp->row_lo, lp->row_hi, lp->var_lb, lp->var_ub, lp->obj,

@@ -117,6 +117,11 @@ struct teccl_lp {
   // lets the PDLP kernels apply A / A^T without reading the stored matrix
   void* te = nullptr;
   void (*te_free)(void*) = nullptr;
+  // source-partitioned solve of a whole single-device TE LP (pdlp.cu
+  // SrcState): this device updates the columns / rows of its sources and
+  // pairs, the capacity rows are summed across devices every iteration
+  void* src = nullptr;
+  void (*src_free)(void*) = nullptr;
 };
 
 // lengths of the vectors the SpMVs gather from, and where the owned part

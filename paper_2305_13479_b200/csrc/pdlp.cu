@@ -997,13 +997,182 @@ __global__ void __launch_bounds__(kThreads, TECCL_SEG_MINB) row_seg_kernel(TeOp 
   }
 }
 
+// ---------------------------------------------------------------------------
+// Source-partitioned solve (SRC): every rank holds the whole single-device TE
+// LP (identical, redundant setup) and updates only the columns of its
+// sources [s0, s1) and pairs [p0, p1) and the rows that touch nothing else
+// (init / conservation / cumulative rows). Commodities couple only through
+// the capacity (and buffer-limit) rows: every iteration each rank sums its
+// sources' x-bar over every capacity row and stores the partial sums straight
+// into every rank's buffer over NVLink (cap_part_kernel), signals, and every
+// rank adds the partials in rank order and applies the capacity rows' dual
+// step itself (cap_fin_kernel) -- identical on all ranks.
+struct OwnMask {
+  int on = 0;
+  uint32_t s0 = 0, s1 = 0, rc0 = 0, rc1 = 0, rm0 = 0, rm1 = 0;  // init, cons, cum rows
+  uint32_t c0 = 0, c1 = 0, q0 = 0, q1 = 0;                        // flow+buffer, Rd/Rc columns
+  __device__ __forceinline__ bool row(uint32_t i) const {
+    return !on || (i >= s0 && i < s1) || (i >= rc0 && i < rc1) || (i >= rm0 && i < rm1);
+  }
+  __device__ __forceinline__ bool col(uint32_t j) const {
+    return !on || (j >= c0 && j < c1) || (j >= q0 && j < q1);
+  }
+};
+
+struct SrcX {
+  double* const* bufs;   // [world] every rank's partial-sum buffers (own included)
+  uint32_t ncap, ncap_e; // capacity + buffer-limit rows; capacity rows (E*K)
+  int world, rank;
+  uint32_t s0, s1;
+  const int4* cap_tasks;
+  int n_cap;
+  Signal sig;
+  Wait wait;
+};
+
+// buffer slot of (parity, value/check, writer rank, row)
+__device__ __forceinline__ int64_t src_slot(const SrcX& X, int parity, int which, int w, uint32_t r) {
+  return ((int64_t)(parity * 2 + which) * X.world + w) * X.ncap + r;
+}
+
+// this rank's columns: flows / buffers of its sources, then its pairs' Rd/Rc
+template <bool CHECK>
+__global__ void __launch_bounds__(kThreads) col_src_kernel(TeOp op, Vecs V, int j_in_chunk, OwnMask M) {
+  __shared__ double sh[32];
+  const uint32_t t = blockIdx.x * kTile + threadIdx.x;
+  const uint32_t n0 = M.c1 - M.c0, n1 = M.q1 - M.q0;
+  const bool on = t < n0 + n1;
+  const uint32_t j = t < n0 ? M.c0 + t : M.q0 + (t - n0);
+  double xj = 0.0, x0 = 0.0, Dj = 1.0, lb = 0.0, ub = 0.0, cj = 0.0, s = 0.0;
+  if (on) {
+    xj = V.x[j];
+    x0 = (double)V.x0[j];
+    Dj = (double)V.D[j];
+  }
+  const PdlpState* st = V.st;
+  if (st->done) return;
+  const double tau = st->tau, refl = st->refl;
+  const double lam = st->lam_tab[j_in_chunk];  // chunks are at most kLamTab iterations
+  if (on) s = te_col(op, j, V.y, lb, ub, cj);
+  double dx = 0.0, dx0 = 0.0;
+  if (on) {
+    const double xt = clampd(xj - tau * Dj * (cj - s), lb, ub);
+    V.xbar[j] = 2.0 * xt - xj;
+    V.x[j] = lam * ((1.0 + refl) * xt - refl * xj) + (1.0 - lam) * x0;
+    if (CHECK) {
+      V.xt[j] = xt;
+      const double w = 1.0 / Dj;
+      dx = (xt - xj) * (xt - xj) * w;
+      dx0 = (xt - x0) * (xt - x0) * w;
+    }
+  }
+  if (CHECK) {
+    double a = block_sum(dx, sh);
+    if (threadIdx.x == 0) V.part[Q_DX * V.pstride + blockIdx.x] = a;
+    a = block_sum(dx0, sh);
+    if (threadIdx.x == 0) V.part[Q_DX0 * V.pstride + blockIdx.x] = a;
+  }
+}
+
+// Partial capacity / buffer-limit row sums over this rank's sources, stored
+// into every rank's buffer (peer memory); the last block signals the peers.
+template <bool CHECK>
+__global__ void __launch_bounds__(kThreads) cap_part_kernel(TeOp op, Vecs V, SrcX X, int parity) {
+  if (V.st->done) return;
+  const int wi = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  bool wrote = false;
+  if (wi < X.n_cap) {
+    const int4 tk = __ldg(X.cap_tasks + wi);
+    const int kind = tk.x & 15, Bv = tk.y, off = tk.w & 0xffffff, cnt = seg_count(tk);
+    const uint32_t K = op.K;
+    for (int h = 0; h < kSegPerLane; ++h) {
+      const int i = lane + 32 * h;
+      if (i >= cnt) continue;
+      uint32_t r, co;  // buffer row, column offset inside a source block
+      if (kind == SEG_CAP) { r = (uint32_t)Bv * K + off + i; co = r; }
+      else { const uint32_t qb = (uint32_t)Bv * (K + 1) + off + i; r = X.ncap_e + qb; co = op.EK + qb; }
+      double a = 0.0, c = 0.0;
+      for (uint32_t s = X.s0; s < X.s1; ++s) {
+        a += __ldg(V.xbar + (size_t)s * op.SB + co);
+        if (CHECK) c += __ldg(V.xt + (size_t)s * op.SB + co);
+      }
+      for (int w = 0; w < X.world; ++w) {
+        X.bufs[w][src_slot(X, parity, 0, X.rank, r)] = a;
+        if (CHECK) X.bufs[w][src_slot(X, parity, 1, X.rank, r)] = c;
+      }
+      wrote = true;
+    }
+  }
+  if (wrote) __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int prev = atomicAdd(X.sig.arrive, 1u);
+    if (prev == gridDim.x - 1) {
+      *X.sig.arrive = 0u;
+      signal_peers(X.sig);
+    }
+  }
+}
+
+// Sum the partials in rank order and take the capacity rows' dual step (every
+// rank, identical); on check iterations also their KKT terms at (A xt, yt).
+// Block partials go to slot blk_off + blockIdx.x; rank 0 alone contributes.
+template <bool CHECK>
+__global__ void __launch_bounds__(kThreads) cap_fin_kernel(TeOp op, Vecs V, SrcX X, int parity,
+                                                           int j_in_chunk, int blk_off) {
+  __shared__ double sh[32];
+  if (V.st->done) return;
+  if (!block_wait_peers(X.wait, V.st)) return;
+  const PdlpState* st = V.st;
+  const double sigma = st->sigma, refl = st->refl;
+  const double lam = st->lam_tab[j_in_chunk];
+  const uint32_t r = blockIdx.x * kTile + threadIdx.x;
+  double dy = 0.0, dy0 = 0.0, rp = 0.0, dobj = 0.0;
+  if (r < X.ncap) {
+    const double* b = X.bufs[X.rank];
+    double a = 0.0;
+    for (int w = 0; w < X.world; ++w) a += b[src_slot(X, parity, 0, w, r)];
+    const bool cap = r < X.ncap_e;
+    const uint32_t i = cap ? op.S + r : op.R_bcap + (r - X.ncap_e);
+    const double lo = -INFINITY, hi = cap ? __ldg(op.d.ecap + r) : op.d.blimit;
+    const double yi = V.y[i], y0 = (double)V.y0[i], Ei = (double)V.E[i];
+    const double yt = dual_step(yi, a, sigma * Ei, lo, hi);
+    V.y[i] = lam * ((1.0 + refl) * yt - refl * yi) + (1.0 - lam) * y0;
+    if (CHECK) {
+      V.yt[i] = yt;
+      if (X.rank == 0) {
+        const double w = 1.0 / Ei;
+        dy = (yt - yi) * (yt - yi) * w;
+        dy0 = (yt - y0) * (yt - y0) * w;
+        double as = 0.0;
+        for (int q = 0; q < X.world; ++q) as += b[src_slot(X, parity, 1, q, r)];
+        const double res = as - clampd(as, lo, hi);
+        rp = res * res;
+        if (yt < 0.0 && isfinite(hi)) dobj = hi * yt;
+      }
+    }
+  }
+  if (CHECK) {
+    double a = block_sum(dy, sh);
+    if (threadIdx.x == 0) V.part[Q_DY * V.pstride + blk_off + blockIdx.x] = a;
+    a = block_sum(dy0, sh);
+    if (threadIdx.x == 0) V.part[Q_DY0 * V.pstride + blk_off + blockIdx.x] = a;
+    a = block_sum(rp, sh);
+    if (threadIdx.x == 0) V.part[Q_RP * V.pstride + blk_off + blockIdx.x] = a;
+    a = block_sum(dobj, sh);
+    if (threadIdx.x == 0) V.part[Q_DOBJ_ROW * V.pstride + blk_off + blockIdx.x] = a;
+  }
+}
+
 // KKT over rows at T(z) = (xt, yt): primal residual of A.xt against the row
 // bounds and the row part of the dual objective.
 template <bool UNIT, int OPK>  // operator: 0 stored SELL, 1 TeOp, 2 EmOp
-__global__ void __launch_bounds__(kThreads) kkt_row_kernel(int32_t m, SellView S, TeOp op, EmOp em, Vecs V) {
+__global__ void __launch_bounds__(kThreads) kkt_row_kernel(int32_t m, SellView S, TeOp op, EmOp em, Vecs V,
+                                                           OwnMask M) {
   __shared__ double sh[32];
   if (V.st->done) return;
-  const int64_t i = (int64_t)blockIdx.x * kTile + threadIdx.x;
+  const int64_t i0 = (int64_t)blockIdx.x * kTile + threadIdx.x;
+  const int64_t i = (i0 < m && M.row((uint32_t)i0)) ? i0 : m;  // rows of other ranks / capacity rows: skipped
   double lo = 0.0, hi = 0.0, s = 0.0;
   if (i < m) {
     if (OPK == 1) {
@@ -1033,10 +1202,12 @@ __global__ void __launch_bounds__(kThreads) kkt_row_kernel(int32_t m, SellView S
 // KKT over columns: reduced costs, dual residual, primal objective and the
 // bound part of the dual objective.
 template <bool UNIT, int OPK>
-__global__ void __launch_bounds__(kThreads) kkt_col_kernel(int32_t n, SellView S, TeOp op, EmOp em, Vecs V) {
+__global__ void __launch_bounds__(kThreads) kkt_col_kernel(int32_t n, SellView S, TeOp op, EmOp em, Vecs V,
+                                                           OwnMask M) {
   __shared__ double sh[32];
   if (V.st->done) return;
-  const int64_t j = (int64_t)blockIdx.x * kTile + threadIdx.x;
+  const int64_t j0 = (int64_t)blockIdx.x * kTile + threadIdx.x;
+  const int64_t j = (j0 < n && M.col((uint32_t)j0)) ? j0 : n;  // columns of other ranks: skipped
   double lb = 0.0, ub = 0.0, cj = 0.0, s = 0.0;
   if (j < n) {
     if (OPK == 1) {
@@ -1567,6 +1738,43 @@ void launch_row(cudaStream_t st, const teccl_lp* lp, const TeOp* te, const EmOp*
     launch_iter(pdl, row_step_kernel<UNIT, DICT, CHECK, false>, V.nb_row, st, (int32_t)lp->m, row_view(lp), V, j);
 }
 
+// Exchange state of a source-partitioned solve (see cap_part_kernel).
+// Arena: partial buffers [2 parities][value, check][world][ncap] doubles |
+// flags[world] | slots[world][kSlots] | seq | arrive; every rank opens every
+// peer's arena through CUDA IPC.
+struct SrcState {
+  int world = 1, rank = 0, device = 0;
+  bool connected = false;
+  OwnMask mask;
+  uint32_t s0 = 0, s1 = 0, p0 = 0, p1 = 0, ncap = 0, ncap_e = 0;
+  int4 *own_tasks = nullptr, *cap_tasks = nullptr;
+  int n_own = 0, n_cap = 0;
+  char* arena = nullptr;
+  int64_t off_flags = 0, off_slots = 0, off_seq = 0, off_arrive = 0, bytes = 0;
+  std::vector<char*> peer_base;
+  double** d_bufs = nullptr;        // [world] buffer base of every rank (own included)
+  double** d_peer_slots = nullptr;  // slot tables of the peers (rank order, self skipped)
+  Signal sig{};
+  Wait wait{};
+  double* slots() const { return (double*)(arena + off_slots); }
+  SrcX view() const {
+    SrcX X{};
+    X.bufs = d_bufs; X.ncap = ncap; X.ncap_e = ncap_e; X.world = world; X.rank = rank;
+    X.s0 = s0; X.s1 = s1; X.cap_tasks = cap_tasks; X.n_cap = n_cap; X.sig = sig; X.wait = wait;
+    return X;
+  }
+  ~SrcState() {
+    cudaSetDevice(device);
+    std::lock_guard<std::mutex> lock(device_mutex());
+    cudaDeviceSynchronize();
+    for (char* b : peer_base)
+      if (b) cudaIpcCloseMemHandle(b);
+    for (void* p : {(void*)d_bufs, (void*)d_peer_slots, (void*)own_tasks, (void*)cap_tasks, (void*)arena})
+      if (p) cudaFree(p);
+  }
+};
+void free_src(void* p) { delete (SrcState*)p; }
+
 struct StepBench {
   int reps;
   double ms_col, ms_row, bytes_col, bytes_row;
@@ -1627,14 +1835,14 @@ void enqueue_chunk(int chunk, cudaStream_t st, const teccl_lp* lp, const TeOp* t
   }
   if (Vr.push.n) X.wait_nbr(st);  // yt ghosts for kkt_col
   if (te) {
-    kkt_row_kernel<UNIT, 1><<<Vr.nb_row, kThreads, 0, st>>>(lp->m, SellView{}, *te, EmOp{}, Vr);
-    kkt_col_kernel<UNIT, 1><<<Vc.nb_col, kThreads, 0, st>>>(lp->n, SellView{}, *te, EmOp{}, Vc);
+    kkt_row_kernel<UNIT, 1><<<Vr.nb_row, kThreads, 0, st>>>(lp->m, SellView{}, *te, EmOp{}, Vr, OwnMask{});
+    kkt_col_kernel<UNIT, 1><<<Vc.nb_col, kThreads, 0, st>>>(lp->n, SellView{}, *te, EmOp{}, Vc, OwnMask{});
   } else if (em) {
-    kkt_row_kernel<UNIT, 2><<<Vr.nb_row, kThreads, 0, st>>>(lp->m, SellView{}, TeOp{}, *em, Vr);
-    kkt_col_kernel<UNIT, 2><<<Vc.nb_col, kThreads, 0, st>>>(lp->n, SellView{}, TeOp{}, *em, Vc);
+    kkt_row_kernel<UNIT, 2><<<Vr.nb_row, kThreads, 0, st>>>(lp->m, SellView{}, TeOp{}, *em, Vr, OwnMask{});
+    kkt_col_kernel<UNIT, 2><<<Vc.nb_col, kThreads, 0, st>>>(lp->n, SellView{}, TeOp{}, *em, Vc, OwnMask{});
   } else {
-    kkt_row_kernel<UNIT, 0><<<Vr.nb_row, kThreads, 0, st>>>(lp->m, row_view(lp), TeOp{}, EmOp{}, Vr);
-    kkt_col_kernel<UNIT, 0><<<Vc.nb_col, kThreads, 0, st>>>(lp->n, col_view(lp), TeOp{}, EmOp{}, Vc);
+    kkt_row_kernel<UNIT, 0><<<Vr.nb_row, kThreads, 0, st>>>(lp->m, row_view(lp), TeOp{}, EmOp{}, Vr, OwnMask{});
+    kkt_col_kernel<UNIT, 0><<<Vc.nb_col, kThreads, 0, st>>>(lp->n, col_view(lp), TeOp{}, EmOp{}, Vc, OwnMask{});
   }
   reduce_publish_kernel<<<1, 1024, 0, st>>>(Vc, X.active() ? X.ds->sig_all : Signal{},
                                             X.active() ? X.ds->d_peer_slots : nullptr);
@@ -1642,6 +1850,43 @@ void enqueue_chunk(int chunk, cudaStream_t st, const teccl_lp* lp, const TeOp* t
   control_kernel<<<1, 32, 0, st>>>(Vc);
   restart_x_kernel<<<grid_for(lp->n), kThreads, 0, st>>>(lp->n, Vc);
   restart_y_kernel<<<grid_for(nrw), kThreads, 0, st>>>(nrw, orr, lp->m, y_w, yt_w, Vr.y0, Vr.st);
+}
+
+// One chunk of a source-partitioned solve: own columns, own rows (segment
+// tasks of this rank), capacity partials to every rank, capacity dual step;
+// then the masked KKT, the cross-rank reduction and the (identical) control.
+template <bool UNIT, bool DICT>
+void enqueue_chunk_src(int chunk, cudaStream_t st, const teccl_lp* lp, const TeOp* te, const SrcState* src,
+                       const Vecs& Vc, const Vecs& Vr, int nb_colsrc, int nb_own, int nb_fin, int blk_off,
+                       double* y_w, double* yt_w) {
+  TeOp own = *te;
+  own.rtask = src->own_tasks;
+  own.n_rtask = src->n_own;
+  const SrcX X = src->view();
+  const int nb_cap = std::max(1, (src->n_cap + 7) / 8);
+  for (int j = 0; j < chunk; ++j) {
+    const bool check = (j == chunk - 1);
+    const int parity = j & 1;
+    if (check) col_src_kernel<true><<<nb_colsrc, kThreads, 0, st>>>(*te, Vc, j, src->mask);
+    else col_src_kernel<false><<<nb_colsrc, kThreads, 0, st>>>(*te, Vc, j, src->mask);
+    if (nb_own > 0) {
+      if (check) row_seg_kernel<true><<<nb_own, kThreads, 0, st>>>(own, Vr, j);
+      else row_seg_kernel<false><<<nb_own, kThreads, 0, st>>>(own, Vr, j);
+    }
+    if (check) cap_part_kernel<true><<<nb_cap, kThreads, 0, st>>>(*te, Vr, X, parity);
+    else cap_part_kernel<false><<<nb_cap, kThreads, 0, st>>>(*te, Vr, X, parity);
+    if (check) cap_fin_kernel<true><<<nb_fin, kThreads, 0, st>>>(*te, Vr, X, parity, j, blk_off);
+    else cap_fin_kernel<false><<<nb_fin, kThreads, 0, st>>>(*te, Vr, X, parity, j, blk_off);
+  }
+  kkt_row_kernel<UNIT, 1><<<(int)((lp->m + kTile - 1) / kTile), kThreads, 0, st>>>(lp->m, SellView{}, *te,
+                                                                                 EmOp{}, Vr, src->mask);
+  kkt_col_kernel<UNIT, 1><<<(int)((lp->n + kTile - 1) / kTile), kThreads, 0, st>>>(lp->n, SellView{}, *te,
+                                                                                 EmOp{}, Vc, src->mask);
+  reduce_publish_kernel<<<1, 1024, 0, st>>>(Vc, src->sig, src->d_peer_slots);
+  wait_kernel<<<1, 32, 0, st>>>(src->wait, Vc.st);
+  control_kernel<<<1, 32, 0, st>>>(Vc);
+  restart_x_kernel<<<grid_for(lp->n), kThreads, 0, st>>>(lp->n, Vc);
+  restart_y_kernel<<<grid_for(lp->m), kThreads, 0, st>>>(lp->m, 0, lp->m, y_w, yt_w, Vr.y0, Vr.st);
 }
 
 // setup-phase all-reduce of `count` quantities laid out as part[k*pstride+b]
@@ -1673,6 +1918,17 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
   const int world = ds ? ds->world : 1, rank = ds ? ds->rank : 0;
   const int64_t ncw = gather_cols(lp), nrw = gather_rows(lp);
   const int64_t oc = own_col_off(lp), orr = own_row_off(lp);
+  // source-partitioned solve: setup is the single-device one (redundant on
+  // every rank); the iteration works on this rank's sources and pairs
+  const SrcState* sp = (const SrcState*)lp->src;
+  if (sp && !sp->connected) {
+    set_error("source-partitioned LP: call teccl_src_export/teccl_src_connect before solving");
+    return TECCL_EINVAL;
+  }
+  const int src_nb_own = sp ? (sp->n_own + 7) / 8 : 0;
+  const int src_nb_fin = sp ? (int)((sp->ncap + kTile - 1) / kTile) : 0;
+  const int src_blk_off = sp ? std::max(nb_row, src_nb_own) : 0;
+  const int src_nb_col = sp ? (int)(((sp->mask.c1 - sp->mask.c0) + (sp->mask.q1 - sp->mask.q0) + kTile - 1) / kTile) : 0;
   Workspace* ws = (Workspace*)lp->pdlp_ws;
   if (!ws) {
     ws = new Workspace();
@@ -1684,6 +1940,7 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
       const TeOp& t = ((TeHold*)lp->te)->op;
       W.pstride = std::max<int64_t>(W.pstride, std::max((t.n_ctask + 7) / 8, (t.n_rtask + 7) / 8));
     }
+    if (sp) W.pstride = std::max<int64_t>(W.pstride, src_blk_off + src_nb_fin);
     W.rstat = W.alloc<double>(m); W.cstat = W.alloc<double>(n);
     // pad slot [n] / [m]: the two-column kernels load pairs unconditionally
     W.D = W.alloc<float>(n + 1); W.E = W.alloc<float>(m + 1);
@@ -1767,6 +2024,7 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
   const EmOp* em_all = (hold && hold->kind == 1) ? &hold->em : nullptr;
   int mf = (te_all || em_all) ? o->matrix_free : 0;
   if (mf == 1) mf = (te_all && lp->n >= kAutoMatrixFreeCols && te_all->K >= 16) ? 4 : 0;
+  if (sp) mf = 2;  // the source-partitioned iteration is matrix-free (col_src / row_seg / cap kernels)
   const TeOp* te = (mf && te_all) ? te_all : nullptr;
   const EmOp* em = (mf && em_all) ? em_all : nullptr;
   const bool seg_col = te && mf == 3, seg_row = te && (mf == 3 || mf == 4);
@@ -1925,11 +2183,22 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
       Vr.wait = ds->wait_nbr;
     }
   }
+  if (sp) {  // cross-rank reductions through the partition's slot tables
+    for (Vecs* v : {&Vc, &Vr}) {
+      v->slots = sp->slots();
+      v->world = sp->world;
+      v->rank = sp->rank;
+      v->nb_col = nb_col;
+      v->nb_row = src_blk_off + src_nb_fin;
+      v->seg = 0;
+    }
+  }
   init_iterates_kernel<<<gr, kThreads, 0, st>>>(n, m, Vi, o->warm_start, x_dev, y_dev);
   nl += 1;
   if (o->warm_start) X.halo(st, {A_Y, A_YT});
   TECCL_CHECK_LAUNCH();
 
+  if (sb && sp) { set_error("step bench is not available for source-partitioned LPs"); return TECCL_EINVAL; }
   if (sb) {  // time the fused iteration kernels alone, CUDA events on this stream
     cudaEvent_t a, b, c2;
     TECCL_CUDA(cudaEventCreate(&a));
@@ -1972,7 +2241,7 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
   }
 
   // --- chunk graph (captured once per LP and chunk length)
-  const int graph_key = chunk * 256 + (o->col_pipeline ? 1 : 0) + (te || em ? 2 : 0) + (o->pdl ? 4 : 0) + 8 * V.seg + 32 * o->fused_halo;
+  const int graph_key = chunk * 256 + (o->col_pipeline ? 1 : 0) + (te || em ? 2 : 0) + (o->pdl ? 4 : 0) + 8 * V.seg + 32 * o->fused_halo + (sp ? 128 : 0);
   if (o->use_graphs && W.gexec && W.graph_chunk != graph_key) {
     cudaGraphExecDestroy(W.gexec);
     W.gexec = nullptr;
@@ -1986,7 +2255,11 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
     cudaStream_t cap;
     TECCL_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
     TECCL_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
-    enqueue_chunk<UNIT, DICT>(chunk, cap, lp, te, em, Vc, Vr, X, y_w, yt_w);
+    if (sp)
+      enqueue_chunk_src<UNIT, DICT>(chunk, cap, lp, te, sp, Vc, Vr, src_nb_col, src_nb_own, src_nb_fin,
+                                    src_blk_off, y_w, yt_w);
+    else
+      enqueue_chunk<UNIT, DICT>(chunk, cap, lp, te, em, Vc, Vr, X, y_w, yt_w);
     TECCL_CUDA(cudaStreamEndCapture(cap, &g));
     TECCL_CUDA(cudaGraphInstantiate(&W.gexec, g, 0));
     TECCL_CUDA(cudaGraphDestroy(g));
@@ -1994,7 +2267,7 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
     W.graph_chunk = graph_key;
   }
   cudaGraphExec_t gexec = o->use_graphs ? W.gexec : nullptr;
-  per_chunk = 2LL * chunk + 6 + (X.active() ? (Vc.push.n || Vr.push.n ? (Vc.wait.npeer ? 2LL : 2LL * chunk + 2) : 4LL * chunk + 1) : 0);
+  per_chunk = sp ? 4LL * chunk + 7 : 2LL * chunk + 6 + (X.active() ? (Vc.push.n || Vr.push.n ? (Vc.wait.npeer ? 2LL : 2LL * chunk + 2) : 4LL * chunk + 1) : 0);
   mark("graph");
 
   // --- iterate: chunks queued `lookahead` deep; the device stops itself
@@ -2023,7 +2296,11 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
       if (gexec) {
         TECCL_CUDA(cudaGraphLaunch(gexec, st));
       } else {
-        enqueue_chunk<UNIT, DICT>(chunk, st, lp, te, em, Vc, Vr, X, y_w, yt_w);
+        if (sp)
+          enqueue_chunk_src<UNIT, DICT>(chunk, st, lp, te, sp, Vc, Vr, src_nb_col, src_nb_own, src_nb_fin,
+                                        src_blk_off, y_w, yt_w);
+        else
+          enqueue_chunk<UNIT, DICT>(chunk, st, lp, te, em, Vc, Vr, X, y_w, yt_w);
       }
       TECCL_CHECK_LAUNCH();
       const int slot = (int)(launched % look);
@@ -2421,5 +2698,139 @@ extern "C" int teccl_dist_connect(teccl_ctx* ctx, teccl_lp* lp, const uint8_t* b
   if (!ps.empty())
     TECCL_CUDA(cudaMemcpy(ds->d_peer_slots, ps.data(), sizeof(double*) * ps.size(), cudaMemcpyHostToDevice));
   ds->connected = true;
+  return TECCL_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Source-partitioned solve of a whole single-device TE LP (SrcState).
+constexpr int kSrcMeta = 8;  // rank, world, ncap, off_flags, off_slots, off_seq, off_arrive, bytes
+constexpr int kSrcBlob = (int)sizeof(cudaIpcMemHandle_t) + kSrcMeta * 8;
+
+extern "C" int teccl_src_setup(teccl_ctx* ctx, teccl_lp* lp, int32_t world, int32_t rank, int64_t* info8) {
+  if (!ctx || !lp || !info8) { set_error("null argument"); return TECCL_EINVAL; }
+  if (world < 1 || rank < 0 || rank >= world || world - 1 > kMaxPeers) { set_error("bad world/rank"); return TECCL_EINVAL; }
+  const TeHold* hold = (const TeHold*)lp->te;
+  if (!hold || hold->kind != 0 || lp->part_world != 1) {
+    set_error("source partition needs a whole LP built by teccl_lp_build_te");
+    return TECCL_EINVAL;
+  }
+  if (lp->src) { set_error("LP already source-partitioned"); return TECCL_EINVAL; }
+  TECCL_CUDA(cudaSetDevice(ctx->device));
+  const TeOp& op = hold->op;
+  const uint32_t S = op.S, P = (uint32_t)op.d.P, K = op.K;
+  std::vector<int> psrc(P);
+  if (P) TECCL_CUDA(cudaMemcpy(psrc.data(), op.d.pair_src, sizeof(int) * P, cudaMemcpyDeviceToHost));
+  for (uint32_t p = 1; p < P; ++p)
+    if (psrc[p] < psrc[p - 1]) { set_error("pairs are not grouped by source"); return TECCL_EINVAL; }
+  SrcState* sp = new SrcState();
+  sp->world = world; sp->rank = rank; sp->device = ctx->device;
+  sp->s0 = (uint32_t)((int64_t)rank * S / world);
+  sp->s1 = (uint32_t)((int64_t)(rank + 1) * S / world);
+  sp->p0 = (uint32_t)(std::lower_bound(psrc.begin(), psrc.end(), (int)sp->s0) - psrc.begin());
+  sp->p1 = (uint32_t)(std::lower_bound(psrc.begin(), psrc.end(), (int)sp->s1) - psrc.begin());
+  OwnMask& M = sp->mask;
+  M.on = 1;
+  M.s0 = sp->s0; M.s1 = sp->s1;
+  M.rc0 = op.R_cons + sp->s0 * op.CB; M.rc1 = op.R_cons + sp->s1 * op.CB;
+  M.rm0 = op.R_cum + sp->p0 * K; M.rm1 = op.R_cum + sp->p1 * K;
+  M.c0 = sp->s0 * op.SB; M.c1 = sp->s1 * op.SB;
+  M.q0 = op.nF + 2 * K * sp->p0; M.q1 = op.nF + 2 * K * sp->p1;
+  sp->ncap_e = op.EK;
+  sp->ncap = op.EK + (op.has_bcap ? (uint32_t)op.d.G * (K + 1) : 0u);
+  // segment tasks: own init / conservation / cumulative rows; all capacity rows
+  std::vector<int4> rt(op.n_rtask), own, cap;
+  if (op.n_rtask)
+    TECCL_CUDA(cudaMemcpy(rt.data(), op.rtask, sizeof(int4) * op.n_rtask, cudaMemcpyDeviceToHost));
+  for (uint32_t s = sp->s0; s < sp->s1; s += kSegTask) {
+    const uint32_t c = std::min<uint32_t>(kSegTask, sp->s1 - s);
+    own.push_back(make_int4(SEG_INIT, 0, (int)s, (int)(s | (c << 24))));
+  }
+  for (const int4& t : rt) {
+    const int kind = t.x & 15, A = t.x >> 4;
+    if (kind == SEG_CONS && (uint32_t)A >= sp->s0 && (uint32_t)A < sp->s1) own.push_back(t);
+    else if (kind == SEG_CUM && (uint32_t)A >= sp->p0 && (uint32_t)A < sp->p1) own.push_back(t);
+    else if (kind == SEG_CAP || kind == SEG_BCAP) cap.push_back(t);
+  }
+  sp->n_own = (int)own.size();
+  sp->n_cap = (int)cap.size();
+  auto up = [](const std::vector<int4>& v, int4** d) -> bool {
+    if (cudaMalloc((void**)d, sizeof(int4) * std::max<size_t>(1, v.size())) != cudaSuccess) return false;
+    return v.empty() || cudaMemcpy(*d, v.data(), sizeof(int4) * v.size(), cudaMemcpyHostToDevice) == cudaSuccess;
+  };
+  if (!up(own, &sp->own_tasks) || !up(cap, &sp->cap_tasks)) { delete sp; set_error("task upload failed"); return TECCL_ECUDA; }
+  auto al = [](int64_t b) { return (b + 255) / 256 * 256; };
+  int64_t off = al(8LL * 4 * world * sp->ncap);
+  sp->off_flags = off; off += al(8LL * world);
+  sp->off_slots = off; off += al(8LL * kSlots * world);
+  sp->off_seq = off; off += 256;
+  sp->off_arrive = off; off += 256;
+  sp->bytes = off;
+  if (cudaMalloc((void**)&sp->arena, off) != cudaSuccess) { delete sp; set_error("cannot allocate the source-partition arena"); return TECCL_ENOMEM; }
+  if (cudaMemset(sp->arena, 0, off) != cudaSuccess) { delete sp; set_error("memset failed"); return TECCL_ECUDA; }
+  lp->src = sp;
+  lp->src_free = free_src;
+  const int64_t v[8] = {sp->s0, sp->s1, sp->p0, sp->p1, M.c0, M.c1, M.q0, M.q1};
+  for (int i = 0; i < 8; ++i) info8[i] = v[i];
+  return TECCL_OK;
+}
+
+extern "C" int teccl_src_export(teccl_ctx* ctx, teccl_lp* lp, uint8_t* blob, int64_t* blob_len) {
+  if (!ctx || !lp || !blob || !blob_len) { set_error("null argument"); return TECCL_EINVAL; }
+  SrcState* sp = (SrcState*)lp->src;
+  if (!sp) { set_error("call teccl_src_setup first"); return TECCL_EINVAL; }
+  TECCL_CUDA(cudaSetDevice(ctx->device));
+  cudaIpcMemHandle_t h;
+  TECCL_CUDA(cudaIpcGetMemHandle(&h, sp->arena));
+  const int64_t meta[kSrcMeta] = {sp->rank, sp->world, sp->ncap, sp->off_flags, sp->off_slots,
+                                   sp->off_seq, sp->off_arrive, sp->bytes};
+  memcpy(blob, &h, sizeof(h));
+  memcpy(blob + sizeof(h), meta, sizeof(meta));
+  *blob_len = kSrcBlob;
+  return TECCL_OK;
+}
+
+extern "C" int teccl_src_connect(teccl_ctx* ctx, teccl_lp* lp, const uint8_t* blobs, int64_t blob_len) {
+  if (!ctx || !lp || !blobs || blob_len != kSrcBlob) { set_error("bad argument"); return TECCL_EINVAL; }
+  SrcState* sp = (SrcState*)lp->src;
+  if (!sp) { set_error("call teccl_src_setup first"); return TECCL_EINVAL; }
+  TECCL_CUDA(cudaSetDevice(ctx->device));
+  const int W = sp->world, me = sp->rank;
+  sp->peer_base.assign(W, nullptr);
+  std::vector<double*> bufs(W), ps;
+  int na = 0;
+  for (int q = 0; q < W; ++q) {
+    int64_t meta[kSrcMeta];
+    memcpy(meta, blobs + (int64_t)q * kSrcBlob + sizeof(cudaIpcMemHandle_t), sizeof(meta));
+    if (meta[0] != q || meta[1] != W || meta[2] != (int64_t)sp->ncap || meta[7] != sp->bytes) {
+      set_error("peer blobs out of rank order or from another LP / world");
+      return TECCL_EINVAL;
+    }
+    char* base = sp->arena;
+    if (q != me) {
+      cudaIpcMemHandle_t h;
+      memcpy(&h, blobs + (int64_t)q * kSrcBlob, sizeof(h));
+      void* ptr = nullptr;
+      TECCL_CUDA(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+      sp->peer_base[q] = (char*)ptr;
+      base = (char*)ptr;
+      ps.push_back((double*)(base + sp->off_slots));
+      sp->sig.peer_flag[na] = (unsigned long long*)(base + sp->off_flags) + me;
+      sp->wait.peer[na] = q;
+      ++na;
+    }
+    bufs[q] = (double*)base;
+  }
+  sp->sig.npeer = na;
+  sp->wait.npeer = na;
+  sp->sig.seq = (unsigned long long*)(sp->arena + sp->off_seq);
+  sp->sig.arrive = (unsigned int*)(sp->arena + sp->off_arrive);
+  sp->wait.flags = (const unsigned long long*)(sp->arena + sp->off_flags);
+  sp->wait.seq = sp->sig.seq;
+  TECCL_CUDA(cudaMalloc((void**)&sp->d_bufs, sizeof(double*) * W));
+  TECCL_CUDA(cudaMemcpy(sp->d_bufs, bufs.data(), sizeof(double*) * W, cudaMemcpyHostToDevice));
+  TECCL_CUDA(cudaMalloc((void**)&sp->d_peer_slots, sizeof(double*) * std::max<size_t>(1, ps.size())));
+  if (!ps.empty())
+    TECCL_CUDA(cudaMemcpy(sp->d_peer_slots, ps.data(), sizeof(double*) * ps.size(), cudaMemcpyHostToDevice));
+  sp->connected = true;
   return TECCL_OK;
 }

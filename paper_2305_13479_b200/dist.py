@@ -181,3 +181,68 @@ def solve_partitioned(t, d, cfg, opts=None, eps_rel: float = 1e-4, max_iters: in
         out["plan"] = plan
     part.close()
     return out
+
+
+SRC_INFO_KEYS = ("s0", "s1", "p0", "p1", "c0", "c1", "q0", "q1")
+
+
+def solve_source_partitioned(t, d, cfg, opts=None, eps_rel: float = 1e-4, max_iters: int = 5_000_000,
+                             device: int | None = None, group=None, gather: bool = False,
+                             pdlp: dict | None = None) -> dict:
+    """Collective call: ONE LP across the ranks of the group, partitioned by
+    source (commodity). Every rank builds the whole LP on its GPU and runs the
+    (identical) setup; in the iteration rank r updates the flows, buffers and
+    reads of sources [s0, s1) and their rows, and the capacity rows -- the only
+    rows shared by the commodities -- are summed across ranks every iteration
+    through peer memory (csrc/pdlp.cu cap_part_kernel / cap_fin_kernel).
+    Returns the (identical) status / objective on every rank and, with
+    gather=True, the full solution in reference column order."""
+    import torch
+    import torch.distributed as dist
+    from .lp import build_from_plan
+    from .solver import SolverOptions, pdlp_options
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    if device is None:
+        device = torch.cuda.current_device()
+    plan = make_plan(t, d, cfg, opts)
+    lp = build_from_plan(plan, device)
+    info = (C.c_int64 * 8)()
+    nat.check(lp.ctx.lib.teccl_src_setup(lp.ctx.handle, lp.handle, int(world), int(rank), info))
+    info = dict(zip(SRC_INFO_KEYS, list(info)))
+    buf = (C.c_uint8 * 512)()
+    blen = C.c_int64()
+    nat.check(lp.ctx.lib.teccl_src_export(lp.ctx.handle, lp.handle, buf, C.byref(blen)))
+    blobs = [None] * world
+    dist.all_gather_object(blobs, bytes(buf[:blen.value]), group=group)
+    joined = b"".join(blobs)
+    arr = (C.c_uint8 * len(joined)).from_buffer_copy(joined)
+    nat.check(lp.ctx.lib.teccl_src_connect(lp.ctx.handle, lp.handle, arr, blen.value))
+    dist.barrier(group=group)
+    x = np.empty(plan.num_vars)
+    y = np.empty(plan.num_rows)
+    res = nat.PdlpResult()
+    o = pdlp_options(SolverOptions(eps_rel=eps_rel, max_iters=max_iters, device=device,
+                                   pdlp=pdlp or {}))
+    nat.check(lp.ctx.lib.teccl_pdlp_solve(lp.ctx.handle, lp.handle, C.byref(o),
+                                          nat.ptr(x, C.c_double), nat.ptr(y, C.c_double),
+                                          C.byref(res)))
+    out = {"status": nat.STATUS.get(res.status, "peer-timeout" if res.status == 5 else "?"),
+           "objective": -res.primal_obj, "iters": int(res.iters), "restarts": int(res.restarts),
+           "rel_gap": res.rel_gap, "rel_primal_res": res.rel_primal_res,
+           "rel_dual_res": res.rel_dual_res, "device_seconds": res.solve_seconds,
+           "kernel_launches": int(res.spmv_launches), "world": world, "rank": rank,
+           "info": dict(info, total_cols=plan.num_vars, total_rows=plan.num_rows)}
+    if gather:
+        own = (info["c0"], info["c1"], x[info["c0"]:info["c1"]].copy(),
+               info["q0"], info["q1"], x[info["q0"]:info["q1"]].copy())
+        pieces = [None] * world
+        dist.all_gather_object(pieces, own, group=group)
+        full = np.empty(plan.num_vars)
+        for c0, c1, xa, q0, q1, xb in pieces:
+            full[c0:c1] = xa
+            full[q0:q1] = xb
+        out["x"] = full
+        out["plan"] = plan
+    lp.close()
+    return out
