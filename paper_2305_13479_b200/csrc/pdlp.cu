@@ -699,11 +699,24 @@ __global__ void __launch_bounds__(kThreads) col_te_kernel(TeOp op, Vecs V, int j
 // blocks per SM, per-column decode. Otherwise 40 registers and one family
 // decode per column pair (te_col2). Measured both ways on the 8- (y 122 MB)
 // and 16-chassis (y 1 GB) LPs, profiles/r01_j_hbm_roofline.md.
-template <bool CHECK, bool WIDE>
-__global__ void __launch_bounds__(kThreads, WIDE ? TECCL_TE2_MINB : TECCL_TE2_MINB_L2) col_te2_kernel(TeOp op, Vecs V, int j_in_chunk) {
+// Column ranges of a source-partitioned rank (RANGE instantiations): pairs of
+// [c0, c1) then of [q0, q1), all four even.
+struct ColRange {
+  uint32_t c0, c1, q0, q1;
+};
+
+template <bool CHECK, bool WIDE, bool RANGE = false>
+__global__ void __launch_bounds__(kThreads, WIDE ? TECCL_TE2_MINB : TECCL_TE2_MINB_L2) col_te2_kernel(TeOp op, Vecs V, int j_in_chunk,
+                                                                                                      ColRange CR = ColRange{}) {
   __shared__ double sh[32];
-  const uint32_t j = 2u * (blockIdx.x * kTile + threadIdx.x);
-  const bool pair = j + 1 < op.n, any = j < op.n;
+  const uint32_t t2 = 2u * (blockIdx.x * kTile + threadIdx.x);
+  uint32_t j = t2, jend = op.n;
+  if (RANGE) {
+    const uint32_t n0 = CR.c1 - CR.c0;
+    j = t2 < n0 ? CR.c0 + t2 : CR.q0 + (t2 - n0);
+    jend = t2 < n0 ? CR.c1 : CR.q1;
+  }
+  const bool pair = j + 1 < jend, any = j < jend;
   // unconditional 16/8-byte loads (x, x0, D have a pad slot [n]; threads
   // past the end load pair 0) kept raw until the epilogue, so the thread
   // issues its table lookups and gathers while they are in flight
@@ -1713,8 +1726,8 @@ void launch_col(cudaStream_t st, const teccl_lp* lp, const TeOp* te, const EmOp*
     launch_iter(pdl, col_seg_kernel<CHECK>, (te->n_ctask + 7) / 8, st, *te, V, j);
   } else if (te && V.col_pipe) {  // col_pipeline selects the two-column variants
     const int g = (int)((te->n + 2 * kTile - 1) / (2 * kTile));
-    if (8.0 * te->m > kL2GatherBytes) launch_iter(pdl, col_te2_kernel<CHECK, true>, g, st, *te, V, j);
-    else launch_iter(pdl, col_te2_kernel<CHECK, false>, g, st, *te, V, j);
+    if (8.0 * te->m > kL2GatherBytes) launch_iter(pdl, col_te2_kernel<CHECK, true>, g, st, *te, V, j, ColRange{});
+    else launch_iter(pdl, col_te2_kernel<CHECK, false>, g, st, *te, V, j, ColRange{});
   } else if (te) {
     launch_iter(pdl, col_te_kernel<CHECK>, (int)((te->n + kTile - 1) / kTile), st, *te, V, j);
   } else if (V.push.n || V.wait.npeer) {  // fused peer exchange compiled in only where used
@@ -1864,11 +1877,27 @@ void enqueue_chunk_src(int chunk, cudaStream_t st, const teccl_lp* lp, const TeO
   own.n_rtask = src->n_own;
   const SrcX X = src->view();
   const int nb_cap = std::max(1, (src->n_cap + 7) / 8);
+  const OwnMask& M = src->mask;
+  const bool pairs = ((M.c0 | M.c1 | M.q0 | M.q1) & 1u) == 0;
+  const bool wide = 8.0 * te->m > kL2GatherBytes;
+  const int nb_pair = (int)((((M.c1 - M.c0) + (M.q1 - M.q0)) / 2 + kTile - 1) / kTile);
   for (int j = 0; j < chunk; ++j) {
     const bool check = (j == chunk - 1);
     const int parity = j & 1;
-    if (check) col_src_kernel<true><<<nb_colsrc, kThreads, 0, st>>>(*te, Vc, j, src->mask);
-    else col_src_kernel<false><<<nb_colsrc, kThreads, 0, st>>>(*te, Vc, j, src->mask);
+    if (pairs) {  // pair-decoded two-column kernel over the rank's ranges
+      const ColRange CR{src->mask.c0, src->mask.c1, src->mask.q0, src->mask.q1};
+      if (wide) {
+        if (check) col_te2_kernel<true, true, true><<<nb_pair, kThreads, 0, st>>>(*te, Vc, j, CR);
+        else col_te2_kernel<false, true, true><<<nb_pair, kThreads, 0, st>>>(*te, Vc, j, CR);
+      } else {
+        if (check) col_te2_kernel<true, false, true><<<nb_pair, kThreads, 0, st>>>(*te, Vc, j, CR);
+        else col_te2_kernel<false, false, true><<<nb_pair, kThreads, 0, st>>>(*te, Vc, j, CR);
+      }
+    } else if (check) {
+      col_src_kernel<true><<<nb_colsrc, kThreads, 0, st>>>(*te, Vc, j, src->mask);
+    } else {
+      col_src_kernel<false><<<nb_colsrc, kThreads, 0, st>>>(*te, Vc, j, src->mask);
+    }
     if (nb_own > 0) {
       if (check) row_seg_kernel<true><<<nb_own, kThreads, 0, st>>>(own, Vr, j);
       else row_seg_kernel<false><<<nb_own, kThreads, 0, st>>>(own, Vr, j);
