@@ -246,3 +246,18 @@ def solve_source_partitioned(t, d, cfg, opts=None, eps_rel: float = 1e-4, max_it
         out["plan"] = plan
     lp.close()
     return out
+
+
+def solve_distributed(t, d, cfg, opts=None, scheme: str = "auto", **kw) -> dict:
+    """One LP across the ranks of the group. scheme "source": partition by
+    commodity (whole LP per rank, fastest while the LP fits one GPU);
+    "epoch": epoch-block row partition (memory-scalable); "auto": "source"
+    when the LP's indices fit the single-device 31-bit limit, else "epoch"."""
+    if scheme == "auto":
+        plan = make_plan(t, d, cfg, opts)
+        scheme = "source" if max(plan.num_vars, plan.num_rows) < (1 << 31) - 1 else "epoch"
+    if scheme == "source":
+        return solve_source_partitioned(t, d, cfg, opts, **kw)
+    if scheme == "epoch":
+        return solve_partitioned(t, d, cfg, opts, **kw)
+    raise ValueError(f"unknown scheme {scheme!r} (auto, source, epoch)")
