@@ -2,6 +2,7 @@
 column map and epoch split."""
 
 import numpy as np
+import pytest
 
 from paper_2305_13479_b200 import EpochConfig, epoch_duration, generate_demand, make_plan
 from paper_2305_13479_b200.dist import em_to_ref_cols, partition_epochs
@@ -32,3 +33,21 @@ def test_partition_epochs_cover_horizon():
         parts = partition_epochs(K, W)
         assert parts[0][0] == 0 and parts[-1][1] == K
         assert all(a[1] == b[0] for a, b in zip(parts, parts[1:]))
+
+
+def test_solve_distributed_scheme_choice(monkeypatch):
+    # auto: source partition while the LP fits the 31-bit single-device
+    # indices, epoch blocks beyond; explicit schemes pass through
+    from paper_2305_13479_b200 import dist as D
+    calls = []
+    monkeypatch.setattr(D, "solve_source_partitioned", lambda *a, **k: calls.append("source") or {})
+    monkeypatch.setattr(D, "solve_partitioned", lambda *a, **k: calls.append("epoch") or {})
+    t = ndv2(2)
+    d = generate_demand("allgather", t, 1, 25000)
+    cfg = EpochConfig(epoch_duration(t, 25000, "fastest", 1), 64, "fastest", 1, 25000)
+    D.solve_distributed(t, d, cfg)
+    D.solve_distributed(t, d, cfg, scheme="epoch")
+    D.solve_distributed(t, d, cfg, scheme="source")
+    assert calls == ["source", "epoch", "source"]
+    with pytest.raises(ValueError):
+        D.solve_distributed(t, d, cfg, scheme="nope")
