@@ -15,7 +15,7 @@ from paper_2305_13479_b200 import (EpochConfig, SolverOptions, check_lp_schedule
                                    epoch_duration, generate_demand, lp_completion_epoch, make_plan, solve)
 from paper_2305_13479_b200.dist import solve_source_partitioned  # noqa: E402
 from paper_2305_13479_b200.lp import build_from_plan  # noqa: E402
-from paper_2305_13479_b200.topology import ndv2  # noqa: E402
+from paper_2305_13479_b200.topology import dgx2, ndv2  # noqa: E402
 
 chassis = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 chunks = int(sys.argv[2]) if len(sys.argv) > 2 else 2
@@ -27,15 +27,18 @@ local = int(os.environ.get("LOCAL_RANK", "0"))
 torch.cuda.set_device(local)
 dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
 rank, world = dist.get_rank(), dist.get_world_size()
-t = ndv2(chassis)
-d = generate_demand("allgather", t, chunks, 25000)
+# TOPO=dgx2 COLL=alltoall for configs[2]-style LPs (default NDv2 AllGather)
+topo = os.environ.get("TOPO", "ndv2")
+coll = os.environ.get("COLL", "allgather")
+t = {"ndv2": ndv2, "dgx2": dgx2}[topo](chassis)
+d = generate_demand(coll, t, chunks, 25000)
 cfg = EpochConfig(epoch_duration(t, d.chunk_size, "fastest", 1), K, "fastest", 1, d.chunk_size)
 t0 = time.perf_counter()
 out = solve_source_partitioned(t, d, cfg, eps_rel=eps, device=local, gather=bool(compare), max_iters=max_iters)
 wall = time.perf_counter() - t0
 secs = torch.tensor([out["device_seconds"]], dtype=torch.float64, device=f"cuda:{local}")
 dist.all_reduce(secs, op=dist.ReduceOp.MAX)
-line = {"workload": f"ALLGATHER {chassis}-chassis NDv2, {chunks} chunk(s), K={K}, source-partitioned",
+line = {"workload": f"{coll.upper()} {chassis}-chassis {topo}, {chunks} chunk(s), K={K}, source-partitioned",
         "n_gpus": world, "eps_rel": eps, "status": out["status"], "iters": out["iters"],
         "objective": out["objective"], "device_seconds_max": float(secs), "wall_s": wall,
         "rel_gap": out["rel_gap"], "info": out["info"]}
