@@ -160,6 +160,19 @@ def roofline_of(sb, peak, peak_kind, lp_key):
                              "algorithmic_bytes_per_launch": sb["bytes_col"] if row_dom else sb["bytes_row"]}}
 
 
+def timed_highs(a, time_limit):
+    """The reference's HiGHS call with its wall time and the host cores it
+    kept busy on average (process CPU time / wall time)."""
+    import resource
+    from oracle import lp_oracle
+    r0 = resource.getrusage(resource.RUSAGE_SELF)
+    r = lp_oracle.solve_highs(a, time_limit=time_limit)
+    r1 = resource.getrusage(resource.RUSAGE_SELF)
+    cpu = (r1.ru_utime - r0.ru_utime) + (r1.ru_stime - r0.ru_stime)
+    r["cores"] = round(cpu / max(r["seconds"], 1e-9), 2)
+    return r
+
+
 def run_reference(args, rank, world):
     """CPU reference arm: oracle restatement of build_lp_model + HiGHS."""
     if rank != 0:
@@ -170,11 +183,12 @@ def run_reference(args, rank, world):
     cap = max(1.0, min(20.0, 200.0 / max(1, args.steps + args.warmup)))
     for _ in range(args.warmup):
         lp_oracle.solve_highs(a, time_limit=cap)
-    times, statuses = [], []
+    times, statuses, cores = [], [], []
     for _ in range(args.steps):
-        r = lp_oracle.solve_highs(a, time_limit=cap)
+        r = timed_highs(a, cap)
         times.append(r["seconds"])
         statuses.append(r["status"])
+        cores.append(r["cores"])
     v = statistics.mean(times)
     censored = any(s != "optimal" for s in statuses)
     sample = (f"scipy.optimize.milp/HiGHS on the full configs[1] LP (as collsched.solver.solve), "
@@ -183,7 +197,8 @@ def run_reference(args, rank, world):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3,
             "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": WORKLOAD, "K": cfg.K, "eps_rel": EPS},
-            "cpu_baseline": {"value": v, "unit": "s", "cores": 1, "kind": "port",
+            "cpu_baseline": {"value": v, "unit": "s", "cores": max(cores), "kind": "port",
+                             "threads_available": os.cpu_count(),
                              "sample": sample, "censored": censored},
             "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -292,8 +307,9 @@ def run_b200(args, rank, world, local_rank):
     if world == 1 and not args.no_cpu_baseline:
         from oracle import lp_oracle
         a = lp_oracle.build_lp_arrays(t, d, cfg.tau, cfg.K, d.chunk_size)
-        r = lp_oracle.solve_highs(a, time_limit=30.0)
-        cpu = {"value": r["seconds"], "unit": "s", "cores": 1, "kind": "port",
+        r = timed_highs(a, 30.0)
+        cpu = {"value": r["seconds"], "unit": "s", "cores": r["cores"], "kind": "port",
+               "threads_available": os.cpu_count(),
                "sample": "scipy.optimize.milp/HiGHS on the same configs[1] LP (the call "
                          "collsched.solver.solve makes), capped at 30 s wall; status=" + r["status"],
                "censored": r["status"] != "optimal"}

@@ -2745,6 +2745,10 @@ extern "C" int teccl_src_setup(teccl_ctx* ctx, teccl_lp* lp, int32_t world, int3
   }
   if (lp->src) { set_error("LP already source-partitioned"); return TECCL_EINVAL; }
   TECCL_CUDA(cudaSetDevice(ctx->device));
+  if (lp->pdlp_ws && lp->ws_free) {  // the partitioned iteration needs more partial slots
+    lp->ws_free(lp->pdlp_ws);
+    lp->pdlp_ws = nullptr;
+  }
   const TeOp& op = hold->op;
   const uint32_t S = op.S, P = (uint32_t)op.d.P, K = op.K;
   std::vector<int> psrc(P);
