@@ -17,6 +17,8 @@ configs[1] itself, whose ~70 MB working set stays in L2 between iterations.
 
 N>1 (torchrun): every rank solves its own instance of the same LP (weak
 scaling, no data-path collective); value = max-over-ranks step time / N.
+`one_lp_across_gpus` (informational, strong scaling): the 8-chassis LP solved
+to 1e-4 once across all N GPUs, partitioned by source (N = 1: one GPU).
 --impl reference times the reference's CPU path (the oracle restatement of
 build_lp_model + scipy HiGHS, exactly the call collsched.solver.solve makes)
 on the host cores, each step capped so the run ends within minutes.
@@ -300,6 +302,31 @@ def run_b200(args, rank, world, local_rank):
                       f"(HBM-resident)")
         roof["ms_per_iteration"] = sbb["ms_col"] + sbb["ms_row"]
         big.close()
+    # --- one LP across all the job's GPUs (strong scaling, informational):
+    # the 8-chassis LP to 1e-4, partitioned by source over the N ranks (one
+    # GPU: the single-device solve), device time max over ranks
+    strong = None
+    if not args.no_strong:
+        bt, bd, bc = big_workload()
+        if dist:
+            from paper_2305_13479_b200.dist import solve_source_partitioned
+            out = solve_source_partitioned(bt, bd, bc, eps_rel=EPS, device=dev)
+            ss = {"status": out["status"], "iters": out["iters"], "objective": out["objective"],
+                  "device_seconds": out["device_seconds"]}
+        else:
+            blp = build_from_plan(make_plan(bt, bd, bc), device=dev)
+            bs = solve(blp, SolverOptions(eps_rel=EPS, time_limit=600.0, max_iters=5_000_000, device=dev))
+            ss = {"status": bs.status, "iters": bs.meta["iters"], "objective": bs.objective,
+                  "device_seconds": bs.meta["device_seconds"]}
+            blp.close()
+        if dist:
+            tt = torch.tensor([ss["device_seconds"]], dtype=torch.float64, device=f"cuda:{dev}")
+            tdist.all_reduce(tt, op=tdist.ReduceOp.MAX)
+            ss["device_seconds"] = float(tt[0])
+        strong = {"lp": f"ALLGATHER 8-chassis NDv2 K={BIG_K} (53.2M columns), eps 1e-4",
+                  "partition": "by source" if dist else "single GPU", "n_gpus": world,
+                  "time_to_1e-4_s": ss["device_seconds"], "iters": ss["iters"],
+                  "status": ss["status"], "objective": ss["objective"]}
     if rank != 0:
         return
     last = sols[-1]
@@ -330,6 +357,7 @@ def run_b200(args, rank, world, local_rank):
         "clocks": clk,
         "gpu_launches": int(launches),
         "parity": parity,
+        "one_lp_across_gpus": strong,
         "solve": {"status": last.status, "iters": last.meta["iters"],
                   "restarts": last.meta["restarts"], "objective": last.objective,
                   "rel_gap": last.meta["rel_gap"], "rel_primal_res": last.meta["rel_primal_res"],
@@ -346,6 +374,8 @@ def main():
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-hbm-roofline", action="store_true")
+    ap.add_argument("--no-strong", action="store_true",
+                    help="skip the one-LP-across-all-GPUs (strong scaling) solve")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
