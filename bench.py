@@ -286,6 +286,18 @@ def run_b200(args, rank, world, local_rank):
         parity["objective_rel_err_at_1e-4"] = abs(sols[-1].objective - gold["objective"]) / abs(gold["objective"])
         parity["reference_completion_epoch"] = gold["completion_epoch"]
         parity["reference_highs_seconds"] = gold["highs_ipm_seconds"]
+        # the 1e-4 KKT gap bounds the duality gap, not the distance to the
+        # optimum (primal residual 7e-5 lets the objective overshoot): the
+        # time until the objective itself is within 1e-4 of the reference's
+        for eps in (3e-5, 1e-5, 3e-6, 1e-6):
+            flush_l2()
+            s3 = solve(lp, SolverOptions(eps_rel=eps, time_limit=600.0, max_iters=5_000_000, device=dev))
+            err = abs(s3.objective - gold["objective"]) / abs(gold["objective"])
+            if err <= 1e-4:
+                parity["time_to_objective_within_1e-4_s"] = s3.meta["device_seconds"]
+                parity["objective_within_1e-4_at"] = {"eps_rel": eps, "iters": s3.meta["iters"],
+                                                      "objective_rel_err": err}
+                break
     # --- roofline of the dominant fused kernel (live CUDA-event timing):
     # on configs[1] (its ~70 MB iteration working set stays in the 126 MB L2
     # between iterations) and on an HBM-resident LP (8-chassis, 3.9 GB moved
