@@ -656,6 +656,42 @@ __device__ __forceinline__ void seg_cols(const TeOp& o, const int4& t, int lane,
   }
 }
 
+#ifndef TECCL_CAP_JOINT
+#define TECCL_CAP_JOINT 1  // capacity rows: sum both entries of a lane together, TECCL_CAP_U sources per round (-6 % on 16 chassis)
+#endif
+#ifndef TECCL_CAP_U
+#define TECCL_CAP_U 4
+#endif
+#ifndef TECCL_CONS_U
+#define TECCL_CONS_U 4     // interior conservation tasks: incident edges per round of gathers
+#endif
+
+// sum_s x[s*SB + q0 + lane + 32h] for the lane's entries (h < kSegPerLane)
+// together, so a round keeps kSegPerLane * TECCL_CAP_U gathers in flight;
+// each entry adds its sources in the same order as te_sum_sources (s
+// ascending, one running sum), so the sums are identical
+__device__ __forceinline__ void seg_sum_sources(const TeOp& o, const double* __restrict__ x, uint32_t q0,
+                                                int lane, int cnt, double (&a)[kSegPerLane]) {
+  uint32_t qh[kSegPerLane];
+#pragma unroll
+  for (int h = 0; h < kSegPerLane; ++h) {
+    a[h] = 0.0;
+    qh[h] = q0 + (uint32_t)min(lane + 32 * h, cnt - 1);  // lanes past the end re-read the last entry
+  }
+  for (uint32_t s0 = 0; s0 < o.S; s0 += TECCL_CAP_U) {
+    double v[kSegPerLane][TECCL_CAP_U];
+#pragma unroll
+    for (int u = 0; u < TECCL_CAP_U; ++u)
+#pragma unroll
+      for (int h = 0; h < kSegPerLane; ++h)
+        v[h][u] = (s0 + u < o.S) ? __ldg(x + (s0 + u) * o.SB + qh[h]) : 0.0;
+#pragma unroll
+    for (int h = 0; h < kSegPerLane; ++h)
+#pragma unroll
+      for (int u = 0; u < TECCL_CAP_U; ++u) a[h] += v[h][u];
+  }
+}
+
 // (A x) for the task's entries lane + 32h, with row bounds.
 __device__ __forceinline__ void seg_rows(const TeOp& o, const int4& t, int lane,
                                          const double* __restrict__ x, double (&a)[kSegPerLane],
@@ -667,11 +703,16 @@ __device__ __forceinline__ void seg_rows(const TeOp& o, const int4& t, int lane,
   for (int h = 0; h < kSegPerLane; ++h) { a[h] = 0.0; lo[h] = 0.0; hi[h] = 0.0; }
   if (kind == SEG_CAP) {                           // cap(e,k): sum_s F(s,e,k)
     const uint32_t q0 = (uint32_t)Bv * K + off;
+#if TECCL_CAP_JOINT
+    seg_sum_sources(o, x, q0, lane, cnt, a);
+#endif
 #pragma unroll
     for (int h = 0; h < kSegPerLane; ++h) {
       const int i = lane + 32 * h;
       if (i < cnt) {
+#if !TECCL_CAP_JOINT
         a[h] = te_sum_sources(o, x, q0 + i);
+#endif
         lo[h] = -INFINITY;
         hi[h] = __ldg(o.d.ecap + q0 + i);
       }
@@ -698,13 +739,13 @@ __device__ __forceinline__ void seg_rows(const TeOp& o, const int4& t, int lane,
     const bool interior = cnt == kSegTask && off >= o.dmax && off + kSegTask <= (int)K - 1;
     if (interior) {
       const double* xb = xs + off + lane;          // term (e*K + c) of epoch off + lane: xb[e*K + c]
-      for (int jb = j0; jb < j1; jb += 4) {
-        int2 e4[4];
+      for (int jb = j0; jb < j1; jb += TECCL_CONS_U) {
+        int2 e4[TECCL_CONS_U];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) e4[u] = (jb + u < j1) ? __ldg(o.incp + jb + u) : make_int2(0, 0);
-        double w[4], v[kSegPerLane][4];
+        for (int u = 0; u < TECCL_CONS_U; ++u) e4[u] = (jb + u < j1) ? __ldg(o.incp + jb + u) : make_int2(0, 0);
+        double w[TECCL_CONS_U], v[kSegPerLane][TECCL_CONS_U];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < TECCL_CONS_U; ++u) {
           w[u] = (jb + u < j1) ? (e4[u].y < 0 ? -1.0 : 1.0) : 0.0;
 #pragma unroll
           for (int h = 0; h < kSegPerLane; ++h) v[h][u] = __ldg(xb + e4[u].x + 32 * h);
@@ -712,7 +753,7 @@ __device__ __forceinline__ void seg_rows(const TeOp& o, const int4& t, int lane,
 #pragma unroll
         for (int h = 0; h < kSegPerLane; ++h)
 #pragma unroll
-          for (int u = 0; u < 4; ++u) a[h] = fma(w[u], v[h][u], a[h]);
+          for (int u = 0; u < TECCL_CONS_U; ++u) a[h] = fma(w[u], v[h][u], a[h]);
       }
     }
     for (int jb = interior ? j1 : j0; jb < j1; jb += 4) {
@@ -758,11 +799,16 @@ __device__ __forceinline__ void seg_rows(const TeOp& o, const int4& t, int lane,
     }
   } else if (kind == SEG_BCAP) {                   // bcap(g,k): sum_s B(s,g,k)
     const uint32_t q0 = o.EK + (uint32_t)Bv * (K + 1) + off;
+#if TECCL_CAP_JOINT
+    seg_sum_sources(o, x, q0, lane, cnt, a);
+#endif
 #pragma unroll
     for (int h = 0; h < kSegPerLane; ++h) {
       const int i = lane + 32 * h;
       if (i < cnt) {
+#if !TECCL_CAP_JOINT
         a[h] = te_sum_sources(o, x, q0 + i);
+#endif
         lo[h] = -INFINITY;
         hi[h] = o.d.blimit;
       }
