@@ -151,6 +151,8 @@ def roofline_of(sb, peak, peak_kind, lp_key):
     ms = sb["ms_row"] if row_dom else sb["ms_col"]
     by = sb["bytes_row"] if row_dom else sb["bytes_col"]
     achieved = by / (ms * 1e-3) / 1e9
+    oms = sb["ms_col"] if row_dom else sb["ms_row"]
+    oby = sb["bytes_col"] if row_dom else sb["bytes_row"]
     return {"bound": "hbm", "kernel": kern, "achieved": achieved, "peak": peak, "peak_kind": peak_kind,
             "unit": "GB/s", "frac": achieved / peak, "traffic": traffic_from_profile(kern, lp_key),
             "ms_per_launch": ms, "algorithmic_bytes_per_launch": by,
@@ -158,8 +160,8 @@ def roofline_of(sb, peak, peak_kind, lp_key):
             else f"matrix-free (mode {sb['matrix_free']})",
             "bound_dictionaries": sb["dict"],
             "other_kernel": {"kernel": cname if row_dom else rname,
-                             "ms_per_launch": sb["ms_col"] if row_dom else sb["ms_row"],
-                             "algorithmic_bytes_per_launch": sb["bytes_col"] if row_dom else sb["bytes_row"]}}
+                             "ms_per_launch": oms, "algorithmic_bytes_per_launch": oby,
+                             "achieved": oby / (oms * 1e-3) / 1e9, "frac": oby / (oms * 1e-3) / 1e9 / peak}}
 
 
 def timed_highs(a, time_limit):
