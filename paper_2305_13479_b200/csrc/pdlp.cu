@@ -53,8 +53,8 @@ namespace teccl {
 #ifndef TECCL_SEG_MINB
 #define TECCL_SEG_MINB 6   // same, row segment kernel (40 registers: -28 % on the 8-chassis LP)
 #endif
-#ifndef TECCL_ROW_PREFETCH
-#define TECCL_ROW_PREFETCH 1  // row segment kernel: L2-prefetch its dense operands, load after the gathers (-9 %)
+#ifndef TECCL_SEG_TPW
+#define TECCL_SEG_TPW 1    // row segment kernel: tasks per warp (descriptors loaded together)
 #endif
 #ifndef TECCL_TE2_MINB
 #define TECCL_TE2_MINB 8  // same, two-column column kernel (32 registers: -8 % on the 16-chassis LP)
@@ -69,6 +69,7 @@ namespace teccl {
 constexpr int kGrid = kSMs * 8;  // blocks of the setup reduction kernels
 constexpr int kNQ = 9;           // partial quantities per check
 constexpr int kSlice = 32;
+constexpr int kSegTPW = TECCL_SEG_TPW;
 constexpr int kTile = kThreads;  // rows (columns) per block of the step kernels
 // auto operator (matrix_free = 1): matrix-free kernels from this many columns
 // up (configs[1], 0.97M columns, runs L2-resident on the stored SELL kernels)
@@ -962,76 +963,59 @@ __global__ void __launch_bounds__(kThreads) col_seg_kernel(TeOp op, Vecs V, int 
 template <bool CHECK>
 __global__ void __launch_bounds__(kThreads, TECCL_SEG_MINB) row_seg_kernel(TeOp op, Vecs V, int j_in_chunk) {
   __shared__ double sh[32];
-  const int wi = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  const int4 tk = (wi < op.n_rtask) ? __ldg(op.rtask + wi) : make_int4(0, 0, 0, 0);
-  const int cnt = seg_count(tk);
-  const uint32_t first = (uint32_t)tk.z;
-  double yi[kSegPerLane];
-  float y0f[kSegPerLane], Ef[kSegPerLane];
-#if TECCL_ROW_PREFETCH
+  const int w0 = (blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5)) * kSegTPW, lane = threadIdx.x & 31;
+  int4 tks[kSegTPW];
+#pragma unroll
+  for (int t = 0; t < kSegTPW; ++t)
+    tks[t] = (w0 + t < op.n_rtask) ? __ldg(op.rtask + w0 + t) : make_int4(0, 0, 0, 0);
   // the dense operands are only prefetched into L2 here and loaded after the
   // gathers: held in registers across seg_rows they were spilled at 40
   // registers, and the spill store waited for the HBM load before any
-  // gather could issue
+  // gather could issue (lanes past a task's end touch its last row)
 #pragma unroll
-  for (int h = 0; h < kSegPerLane; ++h) {
-    const uint32_t r = first + (uint32_t)max(0, min(lane + 32 * h, cnt - 1));
-    prefetch_l2(V.y + r);
-    if ((lane & 1) == 0) { prefetch_l2(V.y0 + r); prefetch_l2(V.E + r); }
-  }
-#else
-  // unconditional loads (lanes past the task's end reload its last row),
-  // kept raw until the epilogue: the gathers issue while they are in flight
+  for (int t = 0; t < kSegTPW; ++t)
 #pragma unroll
-  for (int h = 0; h < kSegPerLane; ++h) {
-    const uint32_t r = first + (uint32_t)max(0, min(lane + 32 * h, cnt - 1));
-    yi[h] = V.y[r];
-    y0f[h] = V.y0[r];
-    Ef[h] = V.E[r];
-  }
-#endif
+    for (int h = 0; h < kSegPerLane; ++h) {
+      const uint32_t r = (uint32_t)tks[t].z + (uint32_t)max(0, min(lane + 32 * h, seg_count(tks[t]) - 1));
+      prefetch_l2(V.y + r);
+      if ((lane & 1) == 0) { prefetch_l2(V.y0 + r); prefetch_l2(V.E + r); }
+    }
   pdl_wait();
   pdl_trigger();
   const PdlpState* st = V.st;
-#if TECCL_ROW_PREFETCH
-  double s[kSegPerLane], lo[kSegPerLane], hi[kSegPerLane];
-  seg_rows(op, tk, lane, V.xbar, s, lo, hi);
-  if (st->done) return;
-  const double sigma = st->sigma, refl = st->refl;
-#else
-  const int done = st->done;
-  const double sigma = st->sigma, refl = st->refl;
-  double s[kSegPerLane], lo[kSegPerLane], hi[kSegPerLane];
-  seg_rows(op, tk, lane, V.xbar, s, lo, hi);
-  if (done) return;
-#endif
-#if TECCL_ROW_PREFETCH
-#pragma unroll
-  for (int h = 0; h < kSegPerLane; ++h) {
-    const uint32_t r = first + (uint32_t)max(0, min(lane + 32 * h, cnt - 1));
-    yi[h] = V.y[r];
-    y0f[h] = V.y0[r];
-    Ef[h] = V.E[r];
-  }
-#endif
-  double y0[kSegPerLane], Ei[kSegPerLane];
-#pragma unroll
-  for (int h = 0; h < kSegPerLane; ++h) { y0[h] = (double)y0f[h]; Ei[h] = (double)Ef[h]; }
-  const double lam = st->lam_tab[j_in_chunk];  // chunks are at most kLamTab iterations
   double dy = 0.0, dy0 = 0.0;
 #pragma unroll
-  for (int h = 0; h < kSegPerLane; ++h) {
-    const int i = lane + 32 * h;
-    if (i < cnt) {
-      const uint32_t r = first + i;
-      const double se = sigma * Ei[h];
-      const double yt = dual_step(yi[h], s[h], se, lo[h], hi[h]);
-      V.y[r] = lam * ((1.0 + refl) * yt - refl * yi[h]) + (1.0 - lam) * y0[h];
-      if (CHECK) {
-        V.yt[r] = yt;
-        const double w = 1.0 / Ei[h];
-        dy += (yt - yi[h]) * (yt - yi[h]) * w;
-        dy0 += (yt - y0[h]) * (yt - y0[h]) * w;
+  for (int t = 0; t < kSegTPW; ++t) {
+    const int4 tk = tks[t];
+    const int cnt = seg_count(tk);
+    const uint32_t first = (uint32_t)tk.z;
+    double s[kSegPerLane], lo[kSegPerLane], hi[kSegPerLane];
+    seg_rows(op, tk, lane, V.xbar, s, lo, hi);
+    if (st->done) return;
+    const double sigma = st->sigma, refl = st->refl;
+    double yi[kSegPerLane], y0[kSegPerLane], Ei[kSegPerLane];
+#pragma unroll
+    for (int h = 0; h < kSegPerLane; ++h) {
+      const uint32_t r = first + (uint32_t)max(0, min(lane + 32 * h, cnt - 1));
+      yi[h] = V.y[r];
+      y0[h] = (double)V.y0[r];
+      Ei[h] = (double)V.E[r];
+    }
+    const double lam = st->lam_tab[j_in_chunk];  // chunks are at most kLamTab iterations
+#pragma unroll
+    for (int h = 0; h < kSegPerLane; ++h) {
+      const int i = lane + 32 * h;
+      if (i < cnt) {
+        const uint32_t r = first + i;
+        const double se = sigma * Ei[h];
+        const double yt = dual_step(yi[h], s[h], se, lo[h], hi[h]);
+        V.y[r] = lam * ((1.0 + refl) * yt - refl * yi[h]) + (1.0 - lam) * y0[h];
+        if (CHECK) {
+          V.yt[r] = yt;
+          const double w = 1.0 / Ei[h];
+          dy += (yt - yi[h]) * (yt - yi[h]) * w;
+          dy0 += (yt - y0[h]) * (yt - y0[h]) * w;
+        }
       }
     }
   }
@@ -1776,7 +1760,7 @@ void launch_row(cudaStream_t st, const teccl_lp* lp, const TeOp* te, const EmOp*
     const int g = (int)((em->m + kTile - 1) / kTile);
     if (V.push.n || V.wait.npeer) launch_iter(pdl, row_em_kernel<CHECK, true>, g, st, *em, V, j);
     else launch_iter(pdl, row_em_kernel<CHECK, false>, g, st, *em, V, j);
-  } else if (te && (V.seg & 2)) launch_iter(pdl, row_seg_kernel<CHECK>, (te->n_rtask + 7) / 8, st, *te, V, j);
+  } else if (te && (V.seg & 2)) launch_iter(pdl, row_seg_kernel<CHECK>, (te->n_rtask + 8 * kSegTPW - 1) / (8 * kSegTPW), st, *te, V, j);
   else if (te) launch_iter(pdl, row_te_kernel<CHECK>, (int)((te->m + kTile - 1) / kTile), st, *te, V, j);
   else if (V.push.n || V.wait.npeer)
     launch_iter(pdl, row_step_kernel<UNIT, DICT, CHECK, true>, V.nb_row, st, (int32_t)lp->m, row_view(lp), V, j);
@@ -1987,7 +1971,7 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
     set_error("source-partitioned LP: call teccl_src_export/teccl_src_connect before solving");
     return TECCL_EINVAL;
   }
-  const int src_nb_own = sp ? (sp->n_own + 7) / 8 : 0;
+  const int src_nb_own = sp ? (sp->n_own + 8 * kSegTPW - 1) / (8 * kSegTPW) : 0;
   const int src_nb_fin = sp ? (int)((sp->ncap + kTile - 1) / kTile) : 0;
   const int src_blk_off = sp ? std::max(nb_row, src_nb_own) : 0;
   const int src_nb_col = sp ? (int)(((sp->mask.c1 - sp->mask.c0) + (sp->mask.q1 - sp->mask.q0) + kTile - 1) / kTile) : 0;

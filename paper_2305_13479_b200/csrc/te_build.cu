@@ -671,6 +671,14 @@ int te_op_tables(const teccl_te_desc* desc, TeHold* h, cudaStream_t st) {
     }
   for (int p = 0; p < P; ++p)
     sntab[(size_t)desc->pair_source[p] * Nn + desc->pair_dst[p]].y = (int)(o.nF + (int64_t)p * 2 * K);
+  std::vector<int4> sefam((size_t)S * E);
+  for (int s = 0; s < S; ++s)
+    for (int e = 0; e < E; ++e) {
+      const int u = desc->edge_src[e], w = desc->edge_dst[e];
+      sefam[(size_t)s * E + e] = make_int4((int)((uint32_t)sntab[(size_t)s * Nn + u].x & kIdxMask),
+                                           sntab[(size_t)s * Nn + w].x, desc->edge_delta[e],
+                                           u == desc->source_node[s] ? 1 : 0);
+    }
   // incident entries in the builder's order: per node, edges ascending, each
   // edge once as leaving (at its source) and once as arriving (at its dst)
   std::vector<int> cnt(Nn + 1, 0);
@@ -726,13 +734,14 @@ int te_op_tables(const teccl_te_desc* desc, TeHold* h, cudaStream_t st) {
   std::vector<double> ninv(K);
   for (int64_t k = 0; k < K; ++k) ninv[k] = -1.0 / (double)(k + 1);
   int4* d4 = nullptr; int2* ds = nullptr; int2* di = nullptr;
-  int4 *dct = nullptr, *drt = nullptr;
+  int4 *dct = nullptr, *drt = nullptr, *dsf = nullptr;
   double* dni = nullptr;
   if (upload(edge4, &d4, st) || upload(sntab, &ds, st) || upload(incp, &di, st) ||
-      upload(ct, &dct, st) || upload(rt, &drt, st) || upload(ninv, &dni, st))
+      upload(ct, &dct, st) || upload(rt, &drt, st) || upload(ninv, &dni, st) || upload(sefam, &dsf, st))
     return TECCL_ECUDA;
-  for (void* p : {(void*)d4, (void*)ds, (void*)di, (void*)dct, (void*)drt, (void*)dni}) h->owned.push_back(p);
-  o.edge4 = d4; o.sntab = ds; o.incp = di;
+  for (void* p : {(void*)d4, (void*)ds, (void*)di, (void*)dct, (void*)drt, (void*)dni, (void*)dsf})
+    h->owned.push_back(p);
+  o.edge4 = d4; o.sntab = ds; o.incp = di; o.sefam = dsf;
   o.ctask = dct; o.rtask = drt; o.neg_inv = dni;
   o.n_ctask = (int)ct.size(); o.n_rtask = (int)rt.size();
   return TECCL_OK;
