@@ -7,7 +7,7 @@
  *   build_lp_model(t, d, cfg, opts)   pkg/src/collsched/lp.py:22-136
  *   solve(m, opts)  -> scipy HiGHS    pkg/src/collsched/solver.py:87-137
  *   lp_completion_epoch(sol)          pkg/src/collsched/lp.py:139-153
- *   simulate(sched, t, d, opts)       pkg/src/collsched/simulator.py:320-470
+ *   simulate(sched, t, d, opts)       pkg/src/collsched/simulator.py:58-235
  *
  * Each entry point below replaces one of those steps. Every argument is a
  * plain pointer or size; host pointers unless the name says `_dev`. All
@@ -38,7 +38,7 @@ extern "C" {
 #define TECCL_OPTIMAL 0        /* all three relative criteria <= eps */
 #define TECCL_ITER_LIMIT 1     /* max_iters reached */
 #define TECCL_TIME_LIMIT 2     /* time_limit reached */
-#define TECCL_PRIMAL_INFEASIBLE 3
+#define TECCL_PRIMAL_INFEASIBLE 3  /* Farkas certificate found (see eps_infeas) */
 #define TECCL_NUMERICAL 4
 #define TECCL_PEER_TIMEOUT 5    /* a peer rank stopped answering (row-partitioned solve) */
 
@@ -139,8 +139,10 @@ int teccl_lp_destroy(teccl_lp* lp);
 /* ---------------------------------------------------------------------------
  * (2)+(3) Restarted Halpern primal-dual hybrid gradient (PDLP family).
  * Replaces the HiGHS call in collsched.solver.solve (solver.py:119-137) for
- * LPs. Termination: relative primal residual, dual residual and duality gap
- * all <= eps_rel (definitions in DESIGN.md).
+ * LPs. Termination: relative duality gap <= eps_rel and relative primal and
+ * dual residuals <= min(eps_rel, eps_res) (definitions in DESIGN.md); primal
+ * infeasibility is certified on the device (eps_infeas) and reported as
+ * TECCL_PRIMAL_INFEASIBLE, the reference's "infeasible" (solver.py:133-135).
  */
 typedef struct {
   double eps_rel;          /* e.g. 1e-4 */
@@ -174,6 +176,15 @@ typedef struct {
   int32_t fused_halo;         /* row-partitioned solves: the half-step kernels store their
                                  boundary outputs into the neighbours' windows over peer
                                  memory and signal, instead of separate halo kernels (1) */
+  double eps_res;             /* > 0: primal and dual residual tolerance min(eps_rel, eps_res),
+                                 the duality gap keeps eps_rel -- the parity bar (gap 1e-4,
+                                 residuals 1e-6); 0: eps_rel for all three (1e-6) */
+  double eps_infeas;          /* primal-infeasibility certificate margin: the solve stops with
+                                 TECCL_PRIMAL_INFEASIBLE once the change of the dual iterate
+                                 between two evaluations is a Farkas ray whose value exceeds
+                                 this fraction of its terms' magnitude; 0 disables (1e-6).
+                                 Single-device solves only */
+  int32_t infeas_every;       /* checks between certificate evaluations (4) */
 } teccl_pdlp_opts;
 
 typedef struct {
@@ -189,6 +200,8 @@ typedef struct {
   double omega;            /* final primal weight */
   double step;             /* eta = 0.998 / ||A_scaled||_2 */
   int64_t spmv_launches;   /* all kernel launches issued by the solve (setup + chunks) */
+  double infeas_cert;      /* last Farkas certificate value / magnitude (> eps_infeas:
+                              TECCL_PRIMAL_INFEASIBLE); 0 before the first evaluation */
 } teccl_pdlp_result;
 
 void teccl_pdlp_default_opts(teccl_pdlp_opts* o);
@@ -229,8 +242,8 @@ int teccl_pdlp_step_bench_opts(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_op
                                int32_t reps, double* out6);
 
 /* ---------------------------------------------------------------------------
- * (4) Exact-integer schedule checker / epoch simulator for a time-expanded
- * LP solution. Replaces simulate() (simulator.py:320-470) for LP schedules:
+ * (4) Exact-integer schedule checker for a time-expanded LP solution: the
+ * flow-level counterpart of simulate() (simulator.py:58-235), on the GPU:
  * flows are quantised to `quantum` units per chunk (int64) and the replay is
  * exact: per (edge,epoch) capacity, per (source,node,epoch) buffer >= 0
  * (causality), switches hold nothing across epochs, every pair's cumulative
@@ -270,6 +283,47 @@ int teccl_schedule_te(const teccl_te_desc* desc, const double* x, double tol, do
                       const int32_t* node_rank, int32_t threads, void** out, int64_t* n_events);
 int teccl_schedule_fetch(void* handle, int32_t* src_slot, int32_t* chunk, int32_t* edge,
                          int32_t* epoch, double* frac);
+
+/* ---------------------------------------------------------------------------
+ * (4b) Event-level schedule replay (host CPU, one thread per commodity).
+ * Replaces simulate() (pkg/src/collsched/simulator.py:58-208 with
+ * _check_capacity :211-223 and _check_switch_rest :226-235) for copy /
+ * no-copy switches: the emitted event list is replayed -- sends of data the
+ * sender does not hold (causality), per-(edge, window) capacity, switch
+ * arrivals left over after their one forwarding epoch, unmet demand. The
+ * caller computes each edge's delay, capacity window and window budget with
+ * the reference's exact rational arithmetic (simulator.py:80-92).
+ */
+typedef struct {
+  int32_t num_nodes;
+  const uint8_t* node_is_switch;  /* [num_nodes] */
+  int32_t num_edges;
+  const int32_t* edge_delta;      /* [E] ceil(alpha/tau) + window widening */
+  const int32_t* edge_window;     /* [E] capacity window in epochs (kap) */
+  const double* edge_budget;      /* [E] float(kap * capacity*tau/chunk) */
+  int64_t num_entries;            /* demanded (source, chunk, destination) entries */
+  const int32_t* entry_source;    /* [num_entries] node index */
+  const int32_t* entry_chunk;
+  const int32_t* entry_dst;       /* node index */
+  int32_t switch_mode;            /* 0 copy, 1 no-copy */
+  double tolerance;               /* SimOptions.tolerance (1e-6) */
+} teccl_sim_desc;
+
+/* Events (source node, chunk, src node, dst node, edge index, epoch,
+ * fraction) in any order; source_rank / node_rank: position of each node in
+ * str() order (the replay order is (epoch, str(source), str(src), str(dst),
+ * chunk), stable). counts4 = {causality, capacity, switch-rest violations,
+ * entries}; teccl_simulate_fetch copies them out -- causality as event ids in
+ * replay order, capacity as (edge, epoch) pairs in (edge, epoch) order,
+ * switch rest as (source, chunk, switch node, usable epoch), per-entry
+ * completion epochs (-1 = unmet) -- and frees the handle. */
+int teccl_simulate(const teccl_sim_desc* desc, int64_t n_events, const int32_t* ev_source,
+                   const int32_t* ev_chunk, const int32_t* ev_src, const int32_t* ev_dst,
+                   const int32_t* ev_edge, const int32_t* ev_epoch, const double* ev_frac,
+                   const int32_t* source_rank, const int32_t* node_rank, int32_t threads,
+                   void** out, int64_t* counts4);
+int teccl_simulate_fetch(void* handle, int64_t* causality, int64_t* capacity, int64_t* sw_rest,
+                         int32_t* entry_done);
 
 #ifdef __cplusplus
 }

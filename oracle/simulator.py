@@ -1,5 +1,5 @@
 """Restatement of the reference's discrete-epoch replay (collsched
-simulator.py:320-470). TEST INFRASTRUCTURE ONLY: used by tests/ to check
+simulator.py:58-235). TEST INFRASTRUCTURE ONLY: used by tests/ to check
 schedules this package emits, never by the product path.
 
 Copy-capable / no-copy switch modes; the hyper-edge mode (legacy switch
@@ -31,20 +31,20 @@ def simulate(events, tau, chunk_size, t, entries, switch_mode="copy", tol=1e-6):
     per_entry=dict)."""
     tau_q = _snap(tau)
     chunk = Fraction(chunk_size)
-    caps = {(e.src, e.dst): _snap(e.capacity) * tau_q / chunk for e in t.edges}   # simulator.py:342-344
+    caps = {(e.src, e.dst): _snap(e.capacity) * tau_q / chunk for e in t.edges}   # simulator.py:80-82
     events = [tuple(e) for e in events]
     whole_only = all(e[5] >= WHOLE for e in events)
     kap = {pair: (max(1, _ceil(1 / c)) if whole_only else 1) for pair, c in caps.items()}
     widen = max(kap.values(), default=1) - 1
     delta = {(e.src, e.dst): _ceil(_snap(e.alpha) / tau_q) + widen for e in t.edges}
-    events.sort(key=lambda e: (e[4], str(e[0]), str(e[2]), str(e[3]), e[1]))      # simulator.py:356-357
+    events.sort(key=lambda e: (e[4], str(e[0]), str(e[2]), str(e[3]), e[1]))      # simulator.py:94-95
     viol = []
     copy_from, frac_pool, sw_arr, deliveries = {}, {}, {}, {}
     for s, c, _ in entries:
         copy_from[(s, c, s)] = 0
     entry_index = set(entries)
 
-    def register(s, c, node, arr, qty):                                           # :381-393
+    def register(s, c, node, arr, qty):                                           # :119-131
         if t.is_switch(node):
             sw_arr.setdefault((s, c, node), []).append(
                 {"usable": arr + 1, "qty": qty, "used": 0.0, "whole": qty >= WHOLE})
@@ -57,7 +57,7 @@ def simulate(events, tau, chunk_size, t, entries, switch_mode="copy", tol=1e-6):
         if (s, c, node) in entry_index:
             deliveries.setdefault((s, c, node), []).append((arr, qty))
 
-    def draw(s, c, node, k, qty):                                                 # :395-425
+    def draw(s, c, node, k, qty):                                                 # :133-163
         if t.is_switch(node):
             recs = [r for r in sw_arr.get((s, c, node), ()) if r["usable"] == k]
             if switch_mode != "no-copy":
@@ -88,11 +88,11 @@ def simulate(events, tau, chunk_size, t, entries, switch_mode="copy", tol=1e-6):
                     return True
         return rem <= tol
 
-    for s, c, i, j, k, f in events:                                               # :427-432
+    for s, c, i, j, k, f in events:                                               # :165-170
         if not draw(s, c, i, k, f):
             viol.append(("causality", f"{i!r} lacks chunk {c} of {s!r}", k))
         register(s, c, j, k + delta[(i, j)], f)
-    load, max_epoch = {}, -1                                                      # :473-485
+    load, max_epoch = {}, -1                                                      # :211-223
     for s, c, i, j, k, f in events:
         load[(i, j, k)] = load.get((i, j, k), 0.0) + f
         max_epoch = max(max_epoch, k)
@@ -103,7 +103,7 @@ def simulate(events, tau, chunk_size, t, entries, switch_mode="copy", tol=1e-6):
             total = sum(load.get((i, j, k2), 0.0) for k2 in range(k - w + 1, k + 1))
             if total > budget * (1 + tol) + tol:
                 viol.append(("capacity", f"({i!r},{j!r})", k))
-    for (s, c, sw), recs in sorted(sw_arr.items(), key=str):                      # :488-497
+    for (s, c, sw), recs in sorted(sw_arr.items(), key=str):                      # :226-235
         for r in recs:
             if switch_mode == "no-copy" or not r["whole"]:
                 if r["qty"] - r["used"] > tol:
@@ -111,7 +111,7 @@ def simulate(events, tau, chunk_size, t, entries, switch_mode="copy", tol=1e-6):
             elif r["used"] == 0.0:
                 viol.append(("switch-buffer", f"chunk {c} of {s!r} rests at {sw!r}", r["usable"]))
     per_entry = {}
-    for key in sorted(entry_index, key=str):                                      # :438-451
+    for key in sorted(entry_index, key=str):                                      # :176-189
         acc, done = 0.0, None
         for arr, qty in sorted(deliveries.get(key, ())):
             acc += qty

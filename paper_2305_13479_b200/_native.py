@@ -23,7 +23,7 @@ EXPORTED = (
     "teccl_lp_export", "teccl_lp_export_csc", "teccl_lp_destroy",
     "teccl_pdlp_default_opts", "teccl_pdlp_solve", "teccl_pdlp_solve_dev",
     "teccl_spmv_bench", "teccl_pdlp_step_bench", "teccl_pdlp_step_bench_opts", "teccl_lp_apply", "teccl_check_te", "teccl_check_te_dev",
-    "teccl_schedule_te", "teccl_schedule_fetch",
+    "teccl_schedule_te", "teccl_schedule_fetch", "teccl_simulate", "teccl_simulate_fetch",
 )
 
 STATUS = {0: "optimal", 1: "iteration-limit", 2: "time-limit", 3: "primal-infeasible",
@@ -55,7 +55,8 @@ class PdlpOpts(C.Structure):
         ("omega_theta", C.c_double), ("omega_scale", C.c_double),
         ("omega_ki", C.c_double), ("omega_kd", C.c_double), ("col_pipeline", C.c_int32),
         ("matrix_free", C.c_int32), ("pdl", C.c_int32),
-        ("fused_halo", C.c_int32),
+        ("fused_halo", C.c_int32), ("eps_res", C.c_double), ("eps_infeas", C.c_double),
+        ("infeas_every", C.c_int32),
     ]
 
 
@@ -65,7 +66,17 @@ class PdlpResult(C.Structure):
         ("primal_obj", C.c_double), ("dual_obj", C.c_double), ("rel_gap", C.c_double),
         ("rel_primal_res", C.c_double), ("rel_dual_res", C.c_double),
         ("solve_seconds", C.c_double), ("omega", C.c_double), ("step", C.c_double),
-        ("spmv_launches", C.c_int64),
+        ("spmv_launches", C.c_int64), ("infeas_cert", C.c_double),
+    ]
+
+
+class SimDesc(C.Structure):
+    _fields_ = [
+        ("num_nodes", C.c_int32), ("node_is_switch", _p(C.c_uint8)), ("num_edges", C.c_int32),
+        ("edge_delta", _p(C.c_int32)), ("edge_window", _p(C.c_int32)),
+        ("edge_budget", _p(C.c_double)), ("num_entries", C.c_int64),
+        ("entry_source", _p(C.c_int32)), ("entry_chunk", _p(C.c_int32)),
+        ("entry_dst", _p(C.c_int32)), ("switch_mode", C.c_int32), ("tolerance", C.c_double),
     ]
 
 
@@ -141,6 +152,12 @@ def load(path: str | None = None):
                                             _p(C.c_int32), C.c_int32, _p(vp), _p(C.c_int64)]),
             "teccl_schedule_fetch": (C.c_int, [vp, _p(C.c_int32), _p(C.c_int32), _p(C.c_int32),
                                                _p(C.c_int32), _p(C.c_double)]),
+            "teccl_simulate": (C.c_int, [_p(SimDesc), C.c_int64, _p(C.c_int32), _p(C.c_int32),
+                                         _p(C.c_int32), _p(C.c_int32), _p(C.c_int32), _p(C.c_int32),
+                                         _p(C.c_double), _p(C.c_int32), _p(C.c_int32), C.c_int32,
+                                         _p(vp), _p(C.c_int64)]),
+            "teccl_simulate_fetch": (C.c_int, [vp, _p(C.c_int64), _p(C.c_int64), _p(C.c_int64),
+                                               _p(C.c_int32)]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)

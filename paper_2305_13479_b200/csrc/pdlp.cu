@@ -67,7 +67,7 @@ namespace teccl {
 #endif
 
 constexpr int kGrid = kSMs * 8;  // blocks of the setup reduction kernels
-constexpr int kNQ = 9;           // partial quantities per check
+constexpr int kNQ = 15;          // partial quantities per check (9 KKT + 6 infeasibility)
 constexpr int kSlice = 32;
 constexpr int kSegTPW = TECCL_SEG_TPW;
 constexpr int kTile = kThreads;  // rows (columns) per block of the step kernels
@@ -78,7 +78,14 @@ constexpr int64_t kAutoMatrixFreeCols = 3000000;
 // hits (126 MB L2 on B200)
 constexpr double kL2GatherBytes = 128.0 * 1024 * 1024;
 
-enum Q { Q_DX = 0, Q_DX0, Q_DY, Q_DY0, Q_RP, Q_DOBJ_ROW, Q_RD, Q_POBJ, Q_DOBJ_COL };
+enum Q { Q_DX = 0, Q_DX0, Q_DY, Q_DY0, Q_RP, Q_DOBJ_ROW, Q_RD, Q_POBJ, Q_DOBJ_COL,
+         // Farkas certificate of the dual-iterate change (infeas_*_kernel): value,
+         // magnitude of its terms, count of needed-but-infinite bounds; rows / columns
+         Q_IC_ROW, Q_IM_ROW, Q_IN_ROW, Q_IC_COL, Q_IM_COL, Q_IN_COL };
+__host__ __device__ constexpr bool row_quantity(int k) {
+  return k == Q_DY || k == Q_DY0 || k == Q_RP || k == Q_DOBJ_ROW || k == Q_IC_ROW || k == Q_IM_ROW ||
+         k == Q_IN_ROW;
+}
 
 struct PdlpState {
   double tau, sigma, omega, eta, refl;
@@ -89,6 +96,10 @@ struct PdlpState {
   long long k_inner, total;
   int have_r0, restart, done, restarts, chunk_len, pad;
   double rel_p, rel_d, gap, pobj, dobj;
+  double eps_res;            // residual tolerance (<= eps)
+  double eps_infeas;         // certificate margin (0: off)
+  double cert;               // last certificate value / magnitude
+  int infeas_every, infeas_due;
   double lam_tab[128];       // Halpern weights (k+1)/(k+2) of the current chunk's iterations
 };
 constexpr int kLamTab = 128;
@@ -286,8 +297,7 @@ __global__ void __launch_bounds__(1024) reduce_publish_kernel(Vecs V, Signal S,
   for (int b = threadIdx.x; b < nbmax; b += blockDim.x) {
 #pragma unroll
     for (int k = 0; k < kNQ; ++k) {
-      const bool row_q = (k == Q_DY || k == Q_DY0 || k == Q_RP || k == Q_DOBJ_ROW);
-      if (b < (row_q ? V.nb_row : V.nb_col)) a[k] += V.part[k * V.pstride + b];
+      if (b < (row_quantity(k) ? V.nb_row : V.nb_col)) a[k] += V.part[k * V.pstride + b];
     }
   }
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
@@ -1271,6 +1281,128 @@ __global__ void __launch_bounds__(kThreads) kkt_col_kernel(int32_t n, SellView S
   if (threadIdx.x == 0) V.part[Q_DOBJ_COL * V.pstride + blockIdx.x] = a;
 }
 
+// ---------------------------------------------------------------------------
+// Primal infeasibility (the reference's "infeasible" status, solver.py:133-135).
+// When the LP has no feasible point, PDHG's dual iterate drifts along a ray
+// v (the infimal displacement of the iteration); every `infeas_every` checks
+// the change of the dual iterate since the previous evaluation, v = yt - yprev,
+// is tested as a Farkas certificate. For every feasible x (r = A x):
+//   v.r >= sum_i (v_i > 0 ? v_i lo_i : v_i hi_i)         (rows, implied bounds)
+//   v.r  = (A^T v).x <= sum_j (g_j > 0 ? g_j ub_j : g_j lb_j),  g = A^T v
+// so C(v) = row part - column part > 0 proves that no feasible x exists. The
+// bounds are the implied ones (implied_*_kernel: valid for every feasible x,
+// finite where the declared bound is not -- F <= capacity, B <= the source's
+// demand, row activity ranges), so a noisy ray still gives a finite value.
+// The solve stops once C(v) > eps_infeas * (sum of |terms|): rounding in the
+// fp64 sums is ~1e-16 of that magnitude, so the margin cannot be met by
+// accident. C(v) is the ray's dual objective (kkt_*_kernel's with c = 0).
+template <int OPK>
+__global__ void __launch_bounds__(kThreads) infeas_row_kernel(int32_t m, Vecs V, const double* __restrict__ loI,
+                                                              const double* __restrict__ hiI,
+                                                              double* __restrict__ yprev,
+                                                              double* __restrict__ dv) {
+  __shared__ double sh[32];
+  const PdlpState* st = V.st;
+  if (st->done || !st->infeas_due) return;
+  const int64_t i = (int64_t)blockIdx.x * kTile + threadIdx.x;
+  double c = 0.0, mag = 0.0, ninf = 0.0;
+  if (i < m) {
+    const double yt = V.yt[i];
+    const double v = yt - yprev[i];
+    yprev[i] = yt;
+    dv[i] = v;
+    const double b = v > 0.0 ? loI[i] : hiI[i];
+    if (v != 0.0) {
+      if (isfinite(b)) { c = v * b; mag = fabs(c); }
+      else ninf = 1.0;
+    }
+  }
+  double a = block_sum(c, sh);
+  if (threadIdx.x == 0) V.part[Q_IC_ROW * V.pstride + blockIdx.x] = a;
+  a = block_sum(mag, sh);
+  if (threadIdx.x == 0) V.part[Q_IM_ROW * V.pstride + blockIdx.x] = a;
+  a = block_sum(ninf, sh);
+  if (threadIdx.x == 0) V.part[Q_IN_ROW * V.pstride + blockIdx.x] = a;
+}
+
+template <bool UNIT, int OPK>
+__global__ void __launch_bounds__(kThreads) infeas_col_kernel(int32_t n, SellView S, TeOp op, Vecs V,
+                                                              const double* __restrict__ ubI,
+                                                              const double* __restrict__ dv) {
+  __shared__ double sh[32];
+  const PdlpState* st = V.st;
+  if (st->done || !st->infeas_due) return;
+  const int64_t j = (int64_t)blockIdx.x * kTile + threadIdx.x;
+  double c = 0.0, mag = 0.0, ninf = 0.0;
+  if (j < n) {
+    double g;
+    if (OPK == 1) {
+      double lb_, ub_, c_;
+      g = te_col(op, (uint32_t)j, dv, lb_, ub_, c_);
+    } else {
+      g = sell_dot<UNIT>(S, (uint32_t)j, dv);
+    }
+    const double b = g > 0.0 ? ubI[j] : V.lb_u[j];
+    if (g != 0.0) {
+      if (isfinite(b)) { c = -g * b; mag = fabs(c); }
+      else ninf = 1.0;
+    }
+  }
+  double a = block_sum(c, sh);
+  if (threadIdx.x == 0) V.part[Q_IC_COL * V.pstride + blockIdx.x] = a;
+  a = block_sum(mag, sh);
+  if (threadIdx.x == 0) V.part[Q_IM_COL * V.pstride + blockIdx.x] = a;
+  a = block_sum(ninf, sh);
+  if (threadIdx.x == 0) V.part[Q_IN_COL * V.pstride + blockIdx.x] = a;
+}
+
+// Implied column upper bounds (setup): the declared ones, and for the
+// time-expanded LP's flows and buffers, which the LP leaves unbounded above
+// (lp.py:47-59), what every feasible point satisfies anyway: a flow
+// F(s,e,k) <= min(capacity(e,k), demand of s) (capacity row lp.py:74-77, all
+// flows >= 0) and a buffer B(s,g,k) <= demand of s (the source's units are
+// conserved, lp.py:67-116, every term >= 0).
+__global__ void implied_col_kernel(int64_t n, const double* __restrict__ ub, TeDev d, int te,
+                                   double* __restrict__ ubI) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    double u = ub[j];
+    if (te && j < (int64_t)d.S * d.SB) {
+      const int64_t s = j / d.SB, r = j - s * d.SB;
+      double t = d.out_units[s];
+      if (r < (int64_t)d.E * d.K) t = fmin(t, d.ecap[r]);  // r = e*K + k, the capacity row's index
+      u = fmin(u, t);
+    }
+    ubI[j] = u;
+  }
+}
+
+// Implied row ranges (setup): [lo, hi] intersected with the activity range of
+// the row over the column box [lb, ubI] (e.g. a capacity row's sum of flows
+// is >= 0).
+template <bool UNIT>
+__global__ void implied_row_kernel(int64_t m, const int64_t* __restrict__ ptr, const uint32_t* __restrict__ idx,
+                                   const double* __restrict__ val, const double* __restrict__ lb,
+                                   const double* __restrict__ ubI, const double* __restrict__ lo,
+                                   const double* __restrict__ hi, double* __restrict__ loI,
+                                   double* __restrict__ hiI) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < m;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    double amin = 0.0, amax = 0.0;
+    for (int64_t p = ptr[r]; p < ptr[r + 1]; ++p) {
+      const uint32_t t = idx[p];
+      const uint32_t j = UNIT ? (t & kIdxMask) : t;
+      const double a = UNIT ? ((t & kSignBit) ? -1.0 : 1.0) : val[p];
+      const double l = lb[j], u = ubI[j];
+      if (a > 0.0) { amin += a * l; amax += a * u; }
+      else if (a < 0.0) { amin += a * u; amax += a * l; }
+    }
+    // (a * inf sums to +-inf; an inf - inf NaN leaves the declared bound)
+    loI[r] = amin > lo[r] ? amin : lo[r];
+    hiI[r] = amax < hi[r] ? amax : hi[r];
+  }
+}
+
 // Sum every rank's reduced partials in rank order (identical on all ranks, so
 // all ranks take the same decisions), evaluate termination, decide restarts
 // and update the primal weight. All of PDLP's control flow.
@@ -1297,9 +1429,17 @@ __device__ void control_decide(Vecs V) {
   st->k_inner += st->chunk_len;
   st->restart = 0;
   if (!isfinite(r) || !isfinite(pobj)) { st->done = 2; return; }
-  if (st->rel_p <= st->eps && st->rel_d <= st->eps && st->gap <= st->eps) {
+  if (st->rel_p <= st->eps_res && st->rel_d <= st->eps_res && st->gap <= st->eps) {
     st->done = 1;
     return;
+  }
+  if (st->infeas_due) {  // this chunk's certificate evaluation (infeas_*_kernel)
+    const double cv = q[Q_IC_ROW] + q[Q_IC_COL], mag = q[Q_IM_ROW] + q[Q_IM_COL];
+    st->cert = mag > 0.0 ? cv / mag : 0.0;
+    if (q[Q_IN_ROW] + q[Q_IN_COL] == 0.0 && mag > 0.0 && cv > st->eps_infeas * mag) {
+      st->done = 5;
+      return;
+    }
   }
   if (!st->have_r0) {
     st->r0 = r;
@@ -1333,7 +1473,12 @@ __device__ void control_decide(Vecs V) {
 __global__ void control_kernel(Vecs V) {
   PdlpState* st = V.st;
   if (st->done) return;
-  if (threadIdx.x == 0) control_decide(V);
+  if (threadIdx.x == 0) {
+    control_decide(V);
+    // certificate evaluation in the next chunk? (every infeas_every checks)
+    const long long c = st->chunk_len > 0 ? st->total / st->chunk_len : 0;
+    st->infeas_due = (st->eps_infeas > 0.0 && st->infeas_every > 0 && (c + 1) % st->infeas_every == 0) ? 1 : 0;
+  }
   __syncwarp();
   // Halpern weights of the next chunk's iterations
   const long long k0 = st->k_inner;
@@ -1641,6 +1786,9 @@ struct Workspace {
   float *D = nullptr, *E = nullptr, *x0 = nullptr, *y0 = nullptr;
   double *x = nullptr, *xt = nullptr, *xbar = nullptr, *y = nullptr, *yt = nullptr;
   double *part = nullptr, *part2 = nullptr, *slots = nullptr;
+  // infeasibility certificate: implied bounds (set up once per LP), previous
+  // dual iterate and the ray candidate (pad slot [m] = 0 for SELL gathers)
+  double *ubI = nullptr, *loI = nullptr, *hiI = nullptr, *yprev = nullptr, *dv = nullptr;
   PdlpState* dst = nullptr;
   int64_t pstride = 0;
   cudaGraphExec_t gexec = nullptr;
@@ -1840,9 +1988,16 @@ struct Exchange {
   }
 };
 
+// Certificate kernels of one chunk (single-device solves; on = false: none).
+struct Infeas {
+  bool on = false;
+  const double *ubI = nullptr, *loI = nullptr, *hiI = nullptr;
+  double *yprev = nullptr, *dv = nullptr;
+};
+
 template <bool UNIT, bool DICT>
 void enqueue_chunk(int chunk, cudaStream_t st, const teccl_lp* lp, const TeOp* te, const EmOp* em, const Vecs& Vc, const Vecs& Vr,
-                   Exchange& X, double* y_w, double* yt_w) {
+                   Exchange& X, double* y_w, double* yt_w, const Infeas& IF) {
   const int64_t nrw = gather_rows(lp), orr = own_row_off(lp);
   for (int j = 0; j < chunk; ++j) {
     const bool check = (j == chunk - 1);
@@ -1873,6 +2028,13 @@ void enqueue_chunk(int chunk, cudaStream_t st, const teccl_lp* lp, const TeOp* t
   } else {
     kkt_row_kernel<UNIT, 0><<<Vr.nb_row, kThreads, 0, st>>>(lp->m, row_view(lp), TeOp{}, EmOp{}, Vr, OwnMask{});
     kkt_col_kernel<UNIT, 0><<<Vc.nb_col, kThreads, 0, st>>>(lp->n, col_view(lp), TeOp{}, EmOp{}, Vc, OwnMask{});
+  }
+  if (IF.on) {  // exits at once unless this chunk evaluates the certificate
+    infeas_row_kernel<0><<<Vr.nb_row, kThreads, 0, st>>>(lp->m, Vr, IF.loI, IF.hiI, IF.yprev, IF.dv);
+    if (te)
+      infeas_col_kernel<UNIT, 1><<<Vc.nb_col, kThreads, 0, st>>>(lp->n, SellView{}, *te, Vc, IF.ubI, IF.dv);
+    else
+      infeas_col_kernel<UNIT, 0><<<Vc.nb_col, kThreads, 0, st>>>(lp->n, col_view(lp), TeOp{}, Vc, IF.ubI, IF.dv);
   }
   reduce_publish_kernel<<<1, 1024, 0, st>>>(Vc, X.active() ? X.ds->sig_all : Signal{},
                                             X.active() ? X.ds->d_peer_slots : nullptr);
@@ -2170,6 +2332,26 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
   TECCL_CHECK_LAUNCH();
 
   mark("power-iter");
+  // --- infeasibility certificate (single device): implied bounds once per LP
+  Infeas IF;
+  IF.on = o->eps_infeas > 0.0 && !ds && !sp && !em_all && !sb;
+  if (IF.on) {
+    if (!W.yprev) {
+      W.ubI = W.alloc<double>(n); W.loI = W.alloc<double>(m); W.hiI = W.alloc<double>(m);
+      W.yprev = W.alloc<double>(m); W.dv = W.alloc<double>(m + 1);
+      if (!W.ubI || !W.loI || !W.hiI || !W.yprev || !W.dv) {
+        set_error("device allocation failed for the infeasibility certificate");
+        return TECCL_ENOMEM;
+      }
+      implied_col_kernel<<<gr, kThreads, 0, st>>>(n, lp->var_ub, te_all ? te_all->d : TeDev{}, te_all ? 1 : 0, W.ubI);
+      implied_row_kernel<UNIT><<<gr, kThreads, 0, st>>>(m, lp->row_ptr, lp->col, lp->val, lp->var_lb, W.ubI,
+                                                         lp->row_lo, lp->row_hi, W.loI, W.hiI);
+      nl += 2;
+      TECCL_CUDA(cudaMemsetAsync(W.dv + m, 0, sizeof(double), st));
+    }
+    TECCL_CUDA(cudaMemsetAsync(W.yprev, 0, sizeof(double) * m, st));
+    IF.ubI = W.ubI; IF.loI = W.loI; IF.hiI = W.hiI; IF.yprev = W.yprev; IF.dv = W.dv;
+  }
   // the setup reductions used the partial slots; the iteration kernels write
   // only as many slots as they have blocks, so start them from zero
   TECCL_CUDA(cudaMemsetAsync(part, 0, sizeof(double) * kNQ * pstride, st));
@@ -2183,6 +2365,10 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
   hs.bnorm = sqrt(bsq_u);
   hs.cnorm = sqrt(csq_u);
   hs.eps = o->eps_rel;
+  hs.eps_res = o->eps_res > 0.0 ? std::min(o->eps_rel, o->eps_res) : o->eps_rel;
+  hs.eps_infeas = IF.on ? o->eps_infeas : 0.0;
+  hs.infeas_every = o->infeas_every > 0 ? o->infeas_every : 4;
+  hs.infeas_due = (IF.on && hs.infeas_every == 1) ? 1 : 0;
   hs.rs_suff = o->restart_sufficient;
   hs.rs_nec = o->restart_necessary;
   hs.rs_art = o->restart_artificial;
@@ -2287,7 +2473,7 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
   }
 
   // --- chunk graph (captured once per LP and chunk length)
-  const int graph_key = chunk * 256 + (o->col_pipeline ? 1 : 0) + (te || em ? 2 : 0) + (o->pdl ? 4 : 0) + 8 * V.seg + 32 * o->fused_halo + (sp ? 128 : 0);
+  const int graph_key = chunk * 512 + (o->col_pipeline ? 1 : 0) + (te || em ? 2 : 0) + (o->pdl ? 4 : 0) + 8 * V.seg + 32 * o->fused_halo + (sp ? 128 : 0) + (IF.on ? 256 : 0);
   if (o->use_graphs && W.gexec && W.graph_chunk != graph_key) {
     cudaGraphExecDestroy(W.gexec);
     W.gexec = nullptr;
@@ -2305,7 +2491,7 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
       enqueue_chunk_src<UNIT, DICT>(chunk, cap, lp, te, sp, Vc, Vr, src_nb_col, src_nb_own, src_nb_fin,
                                     src_blk_off, y_w, yt_w);
     else
-      enqueue_chunk<UNIT, DICT>(chunk, cap, lp, te, em, Vc, Vr, X, y_w, yt_w);
+      enqueue_chunk<UNIT, DICT>(chunk, cap, lp, te, em, Vc, Vr, X, y_w, yt_w, IF);
     TECCL_CUDA(cudaStreamEndCapture(cap, &g));
     TECCL_CUDA(cudaGraphInstantiate(&W.gexec, g, 0));
     TECCL_CUDA(cudaGraphDestroy(g));
@@ -2313,7 +2499,7 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
     W.graph_chunk = graph_key;
   }
   cudaGraphExec_t gexec = o->use_graphs ? W.gexec : nullptr;
-  per_chunk = sp ? 4LL * chunk + 7 : 2LL * chunk + 6 + (X.active() ? (Vc.push.n || Vr.push.n ? (Vc.wait.npeer ? 2LL : 2LL * chunk + 2) : 4LL * chunk + 1) : 0);
+  per_chunk = sp ? 4LL * chunk + 7 : 2LL * chunk + 6 + (IF.on ? 2 : 0) + (X.active() ? (Vc.push.n || Vr.push.n ? (Vc.wait.npeer ? 2LL : 2LL * chunk + 2) : 4LL * chunk + 1) : 0);
   mark("graph");
 
   // --- iterate: chunks queued `lookahead` deep; the device stops itself
@@ -2346,7 +2532,7 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
           enqueue_chunk_src<UNIT, DICT>(chunk, st, lp, te, sp, Vc, Vr, src_nb_col, src_nb_own, src_nb_fin,
                                         src_blk_off, y_w, yt_w);
         else
-          enqueue_chunk<UNIT, DICT>(chunk, st, lp, te, em, Vc, Vr, X, y_w, yt_w);
+          enqueue_chunk<UNIT, DICT>(chunk, st, lp, te, em, Vc, Vr, X, y_w, yt_w, IF);
       }
       TECCL_CHECK_LAUNCH();
       const int slot = (int)(launched % look);
@@ -2366,6 +2552,7 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
     if (last.done == 1) { status = TECCL_OPTIMAL; stop = true; }
     else if (last.done == 2) { status = TECCL_NUMERICAL; stop = true; }
     else if (last.done == 4) { status = TECCL_PEER_TIMEOUT; stop = true; }
+    else if (last.done == 5) { status = TECCL_PRIMAL_INFEASIBLE; stop = true; }
     else if (polled >= max_chunks) { status = TECCL_ITER_LIMIT; stop = true; }
     else if (!X.active()) {  // ranks must stop together: only iteration caps in multi-GPU
       const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
@@ -2381,6 +2568,7 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
   TECCL_CUDA(cudaMemcpyAsync(&last, dst, sizeof(PdlpState), cudaMemcpyDeviceToHost, st));
   TECCL_CUDA(cudaStreamSynchronize(st));
   if (last.done == 1) status = TECCL_OPTIMAL;
+  if (last.done == 5) status = TECCL_PRIMAL_INFEASIBLE;
   if (last.done == 3) last.done = 0;
 
   mark("iterate");
@@ -2404,6 +2592,7 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
   res->omega = last.omega;
   res->step = hs.eta;
   res->spmv_launches = nl_setup + 1 + launched * per_chunk;
+  res->infeas_cert = last.cert;
   return TECCL_OK;
 }
 
@@ -2443,6 +2632,9 @@ extern "C" void teccl_pdlp_default_opts(teccl_pdlp_opts* o) {
   o->matrix_free = 1;  // auto: stored SELL while L2-resident (configs[1]), matrix-free above
   o->pdl = 1;
   o->fused_halo = 1;
+  o->eps_res = 1e-6;
+  o->eps_infeas = 1e-6;
+  o->infeas_every = 4;
 }
 
 extern "C" int teccl_pdlp_solve_dev(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* opts,

@@ -317,8 +317,12 @@ def build_from_plan(plan: LpPlan, device: int = 0, slot: int = 0) -> DeviceLP:
 def lp_completion_epoch(sol, tol: float = TOL) -> int:
     """Earliest epoch by which every pair's cumulative reads meet its demand
     (reference lp.py:139-153), vectorised over pairs."""
-    plan = sol.model.plan
-    rc = plan.rc_matrix(sol.x)
+    return completion_of(sol.model.plan, sol.x, tol)
+
+
+def completion_of(plan: "LpPlan", x, tol: float = TOL) -> int:
+    """lp_completion_epoch of a solution vector x of `plan`'s LP."""
+    rc = plan.rc_matrix(x)
     need = plan.pair_units - tol * np.maximum(1.0, plan.pair_units)
     ok = rc >= need[:, None]
     if not ok.any(axis=1).all():
@@ -329,22 +333,32 @@ def lp_completion_epoch(sol, tol: float = TOL) -> int:
 
 
 def feasibility_gap(plan: LpPlan, device: int = 0, eps_rel: float = 1e-7,
-                    max_iters: int = 2_000_000) -> float:
+                    max_iters: int = 2_000_000, time_limit: float = 300.0) -> float:
     """Demand (in chunks) the horizon cannot deliver: solve the phase-1 LP --
     same rows, final cumulative reads free in [0, u], maximise their sum --
     and return sum(u) minus its optimum (0 up to solver accuracy iff the
-    reference's LP at this horizon is feasible)."""
+    reference's LP at this horizon is feasible). A phase-1 solve that does not
+    converge raises SolverBackendError, like the reference's timed-out
+    horizon probe (solver.py:159-160); its iterate is never a verdict."""
     from dataclasses import replace
-    from .solver import SolverOptions, solve
+    from .errors import SolverBackendError
+    from .solver import OPTIMAL, SolverOptions, solve
     p1 = replace(plan, phase1=True, _desc=None)
     lp = build_from_plan(p1, device)
-    sol = solve(lp, SolverOptions(eps_rel=eps_rel, max_iters=max_iters, device=device))
-    lp.close()
+    try:
+        sol = solve(lp, SolverOptions(eps_rel=eps_rel, max_iters=max_iters, time_limit=time_limit,
+                                      device=device))
+    finally:
+        lp.close()
+    if sol.status != OPTIMAL:
+        raise SolverBackendError(f"phase-1 probe did not converge at K={plan.K} ({sol.status})")
     return float(plan.pair_units.sum() - sol.objective)
 
 
-def horizon_feasible(plan: LpPlan, device: int = 0) -> bool:
-    """Feasibility verdict for min_feasible_horizon: unmet demand above
-    max(1e-3 chunk, 1e-6 of the total) means infeasible."""
-    gap = feasibility_gap(plan, device)
+def horizon_feasible(plan: LpPlan, device: int = 0, max_iters: int = 2_000_000,
+                     time_limit: float = 300.0) -> bool:
+    """Phase-1 feasibility verdict: unmet demand above max(1e-3 chunk, 1e-6
+    of the total) means infeasible. (solve() itself certifies infeasibility;
+    this is the independent cross-check the tests use.)"""
+    gap = feasibility_gap(plan, device, max_iters=max_iters, time_limit=time_limit)
     return gap <= max(1e-3, 1e-6 * float(plan.pair_units.sum()))

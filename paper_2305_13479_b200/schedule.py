@@ -18,7 +18,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from .errors import ConservationError, SolverBackendError, ValidationError
-from .lp import TOL, LpPlan
+from .lp import TOL, LpPlan, completion_of
 
 
 @dataclass(frozen=True)
@@ -68,7 +68,6 @@ def lp_rates_to_schedule(sol, t=None, d=None, cfg=None) -> Schedule:
 def schedule_with_flows(sol) -> tuple:
     """(Schedule, x): the schedule and the exactly conserving flow vector its
     events were peeled from (the repaired / polished solution), for replay."""
-    from .lp import lp_completion_epoch
     if not sol.feasible:
         raise ValidationError(f"cannot schedule a solution with status {sol.status}")
     plan: LpPlan = sol.model.plan
@@ -92,7 +91,9 @@ def schedule_with_flows(sol) -> tuple:
                 "polish_iters": pol.meta["iters"], "polish_device_s": pol.meta["device_seconds"]}
         events, x = _decompose_solution(plan, pol.x)
         sol = pol
-    sched = Schedule(tau=plan.cfg.tau, events=tuple(events), completion_epoch=lp_completion_epoch(sol),
+    # finish time of the flows the events were peeled from (the repaired /
+    # polished x), the reference's lp_completion_epoch rule (lp.py:139-153)
+    sched = Schedule(tau=plan.cfg.tau, events=tuple(events), completion_epoch=completion_of(plan, x),
                      chunk_size=plan.demand.chunk_size, meta=meta)
     return sched, x
 
@@ -101,25 +102,44 @@ POLISH_EPS = 1e-8
 
 
 def _decompose_solution(plan: LpPlan, x) -> tuple:
+    """(events, x'): the decomposition and the flow vector it was peeled from.
+
+    1. A near-vertex solution (every pool's deficit <= RAW_OK, far below the
+       reference's TOL) is decomposed exactly as the reference does it: the
+       raw x with TOL = 1e-6 thresholds. For a unique optimum this gives the
+       reference's event list (GPU solutions carry ~1e-9 noise, all below TOL).
+    2. Otherwise (a looser first-order point) the flows are repaired to
+       conserve exactly and peeled with the reference's TOL, then with DUST if
+       TOL-sized remnants block a path.
+    """
     x = np.asarray(x, dtype=np.float64)
-    tol = TOL
-    if max_deficit(plan, x) > EXACT:  # first-order solution: make every read traceable
-        x = repair_flows(plan, x)
-        tol = DUST
-        # reads only shrink in the repair: a pair whose reads no longer add up
-        # to its demand would end in a residue -- say so before peeling
-        if plan.P and float((plan.pair_units - plan.rd_matrix(x).sum(axis=1)).max()) > TOL:
-            raise ConservationError("repaired flows deliver less than the demand")
+    if max_deficit(plan, x) <= RAW_OK:
+        try:
+            return _native_or_residue(plan, x, TOL), x
+        except ConservationError:
+            pass
+    xr = repair_flows(plan, x)
+    # reads only shrink in the repair: a pair whose reads no longer add up to
+    # its demand would end in a residue -- say so before peeling
+    if plan.P and float((plan.pair_units - plan.rd_matrix(xr).sum(axis=1)).max()) > TOL:
+        raise ConservationError("repaired flows deliver less than the demand")
     try:
-        return decompose_native(plan, x, tol), x
+        return _native_or_residue(plan, xr, TOL), xr
+    except ConservationError:
+        return _native_or_residue(plan, xr, DUST), xr
+
+
+def _native_or_residue(plan: LpPlan, x: np.ndarray, tol: float) -> list:
+    try:
+        return decompose_native(plan, x, tol)
     except SolverBackendError as exc:  # the native decomposition reports residues as errors
         if "conservation residue" in str(exc) or "did not converge" in str(exc):
             raise ConservationError(str(exc)) from exc
         raise
 
 
-EXACT = 1e-9  # deficits below this: leave the solution untouched (vertex solutions)
-DUST = 1e-12  # peel threshold after repair (exact conservation, no 1e-6 dust)
+RAW_OK = 1e-7  # pool deficits up to this: decompose x as is (reference procedure)
+DUST = 1e-12  # peel threshold of last resort on repaired flows
 
 
 def _pool_terms(plan: LpPlan, F, k, S, Nn, pair_of):

@@ -23,7 +23,7 @@ for eps in (1e-4, 1e-8):
     t0 = time.perf_counter(); dfc = S.max_deficit(plan, x); out["max_deficit_s"] = time.perf_counter() - t0
     out["deficit"] = dfc
     tol = S.TOL
-    if dfc > S.EXACT:
+    if dfc > S.RAW_OK:
         t0 = time.perf_counter(); x = S.repair_flows(plan, x); out["repair_s"] = time.perf_counter() - t0
         tol = S.DUST
     try:
