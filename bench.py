@@ -1,11 +1,16 @@
 """Benchmark: time-to-1e-4-gap of the TE-CCL LP on B200 (BASELINE.json metric).
 
-A "step" is one full PDLP solve, to relative KKT tolerance 1e-4, of the
-configs[1] LP: AllGather on 2-chassis NDv2 (16 GPUs + 1 switch, 2 chunks per
-GPU, 25 KB chunks, fastest-link epochs, store-and-forward buffers), whose
-constraint matrix is already resident in HBM when the timed region starts.
-`e2e` repeats the step through the public API from host buffers: host plan
--> H2D tables -> device build -> solve -> D2H solution.
+A "step" is one full PDLP solve of the configs[1] LP -- AllGather on
+2-chassis NDv2 (16 GPUs + 1 switch, 2 chunks per GPU, 25 KB chunks,
+fastest-link epochs, store-and-forward buffers) -- to north_star's parity
+bar: relative duality gap <= 1e-4 AND relative primal and dual residuals
+<= 1e-6 (the solver's default "optimal"), with the constraint matrix already
+resident in HBM when the timed region starts. Every timed solve's objective
+is compared with the reference optimum (tests/golden/full_size.json). `e2e`
+repeats the step through the public API from host buffers: host plan -> H2D
+tables -> device build -> solve -> D2H solution. `value_kkt_1e-4`: the same
+solve stopped at the looser all-three-criteria 1e-4 KKT point (round 1's
+headline, for continuity).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 
@@ -16,12 +21,17 @@ large-LP (matrix-free) kernels; `roofline_l2_resident`: the same for
 configs[1] itself, whose ~70 MB working set stays in L2 between iterations.
 
 N>1 (torchrun): every rank solves its own instance of the same LP (weak
-scaling, no data-path collective); value = max-over-ranks step time / N.
+scaling, no data-path collective): `value` is the per-LP time, max over
+ranks (not divided by N); `throughput_lps_per_s` = N / value.
 `one_lp_across_gpus` (informational, strong scaling): the 8-chassis LP solved
-to 1e-4 once across all N GPUs, partitioned by source (N = 1: one GPU).
+once across all N GPUs, partitioned by source (N = 1: one GPU).
+`reference_uncensored` (N = 1): the configs[0] family (1-chassis NDv2
+AllGather) at horizons where the reference's HiGHS finishes, both arms on
+the same LP in the same run.
 --impl reference times the reference's CPU path (the oracle restatement of
 build_lp_model + scipy HiGHS, exactly the call collsched.solver.solve makes)
-on the host cores, each step capped so the run ends within minutes.
+on the host cores, each step capped so the run ends within minutes (the
+value is then a censored lower bound, flagged in the line).
 """
 
 from __future__ import annotations
@@ -41,7 +51,8 @@ METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
 WORKLOAD = ("ALLGATHER on 2-chassis NDv2 (16 GPUs + switch, 2 chunks/GPU, 25 KB chunks), "
             "copy-free time-expanded LP, fastest-link epochs, store-and-forward buffers")
 K_EPOCHS = 530        # horizon of the benchmarked LP (feasible >= 519)
-EPS = 1e-4
+EPS = 1e-4            # relative duality gap
+EPS_RES = 1e-6        # relative primal / dual residuals (north_star parity bar)
 REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
            0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
            0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
@@ -177,6 +188,13 @@ def timed_highs(a, time_limit):
     return r
 
 
+def bench_config(cfg):
+    """The `config` object both arms print (identical keys and values)."""
+    return {"workload": WORKLOAD, "K": cfg.K, "eps_rel": EPS, "eps_res": EPS_RES,
+            "criterion": "gap <= eps_rel and primal/dual residuals <= eps_res (relative)",
+            "l2": "flushed (256 MiB write) before every GPU step"}
+
+
 def run_reference(args, rank, world):
     """CPU reference arm: oracle restatement of build_lp_model + HiGHS."""
     if rank != 0:
@@ -184,9 +202,9 @@ def run_reference(args, rank, world):
     from oracle import lp_oracle
     t, d, cfg = workload()
     a = lp_oracle.build_lp_arrays(t, d, cfg.tau, cfg.K, d.chunk_size)
-    cap = max(1.0, min(20.0, 200.0 / max(1, args.steps + args.warmup)))
-    for _ in range(args.warmup):
-        lp_oracle.solve_highs(a, time_limit=cap)
+    cap = max(2.0, min(60.0, 240.0 / max(1, args.steps)))
+    for _ in range(args.warmup):  # warm-up: imports / page-in only
+        lp_oracle.solve_highs(a, time_limit=1.0)
     times, statuses, cores = [], [], []
     for _ in range(args.steps):
         r = timed_highs(a, cap)
@@ -200,16 +218,62 @@ def run_reference(args, rank, world):
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3,
             "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": WORKLOAD, "K": cfg.K, "eps_rel": EPS},
+            "data": "synthetic", "config": bench_config(cfg),
+            "censored_lower_bound": censored,
             "cpu_baseline": {"value": v, "unit": "s", "cores": max(cores), "kind": "port",
                              "threads_available": os.cpu_count(),
                              "sample": sample, "censored": censored},
             "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    if censored:
+        line["note"] = ("every step hit its time cap: value is a lower bound on the reference's "
+                        "time (HiGHS IPM + crossover needs 1348 s on 8 cores, tests/golden/full_size.json)")
     print(json.dumps(line), flush=True)
 
 
+def reference_uncensored(dev, horizons=(8, 64, 512), cap=120.0):
+    """configs[0] family (ALLGATHER, 1-chassis NDv2, 1 chunk) at horizons where
+    HiGHS finishes: the reference's path (oracle build + HiGHS) and this
+    engine's public API (host plan -> device build -> solve at the parity
+    bar -> D2H), same LP, same run; the reference's cores are measured."""
+    from oracle import lp_oracle
+    from paper_2305_13479_b200 import (EpochConfig, SolverOptions, epoch_duration, generate_demand,
+                                       lp_completion_epoch, make_plan, solve)
+    from paper_2305_13479_b200.lp import build_from_plan
+    from paper_2305_13479_b200.topology import ndv2
+    t = ndv2(1)
+    d = generate_demand("allgather", t, 1, 25000)
+    tau = epoch_duration(t, 25000, "fastest", 1)
+    out = []
+    for K in horizons:
+        cfg = EpochConfig(tau, K, "fastest", 1, 25000)
+        t0 = time.perf_counter()
+        a = lp_oracle.build_lp_arrays(t, d, tau, K, 25000)
+        build_s = time.perf_counter() - t0
+        r = timed_highs(a, cap)
+        build_from_plan(make_plan(t, d, cfg), device=dev).close()  # warm-up
+        t0 = time.perf_counter()
+        lp = build_from_plan(make_plan(t, d, cfg), device=dev)
+        sol = solve(lp, SolverOptions(device=dev))
+        gpu_s = time.perf_counter() - t0
+        rec = {"K": K, "cols": len(a["var_lb"]), "rows": len(a["row_lo"]),
+               "reference_s": build_s + r["seconds"], "reference_status": r["status"],
+               "reference_cores": r["cores"], "gpu_e2e_s": gpu_s, "gpu_status": sol.status,
+               "gpu_iters": sol.meta["iters"]}
+        if r["status"] == "optimal":
+            rec["objective_rel_err"] = abs(sol.objective - r["objective"]) / abs(r["objective"])
+            rec["completion_epoch_ref_gpu"] = [lp_oracle.completion_epoch(a, r["x"]),
+                                               lp_completion_epoch(sol, tol=1e-5)]
+            rec["speedup"] = rec["reference_s"] / gpu_s
+        out.append(rec)
+        lp.close()
+    return {"workload": "configs[0]: ALLGATHER on 1-chassis NDv2, 1 chunk/GPU, fastest-link epochs",
+            "reference": "oracle build_lp_model restatement + scipy milp/HiGHS (the call collsched makes)",
+            "gpu": "public API e2e: host plan -> device build -> solve (parity bar) -> D2H",
+            "rows": out}
+
+
 def run_b200(args, rank, world, local_rank):
-    import numpy as np
+    import numpy as np  # noqa: F401
     import torch
     from paper_2305_13479_b200 import SolverOptions, make_plan, solve
     from paper_2305_13479_b200.lp import build_from_plan
@@ -222,8 +286,9 @@ def run_b200(args, rank, world, local_rank):
     t, d, cfg = workload()
     plan = make_plan(t, d, cfg)
     lp = build_from_plan(plan, device=dev)
-    opts = SolverOptions(eps_rel=EPS, time_limit=600.0, max_iters=5_000_000, device=dev)
+    opts = SolverOptions(eps_rel=EPS, eps_res=EPS_RES, time_limit=600.0, max_iters=5_000_000, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{dev}")
+    gold = golden_for(cfg.K)
 
     def flush_l2():
         flush.fill_(1.0)
@@ -250,6 +315,7 @@ def run_b200(args, rank, world, local_rank):
     clk = clocks.stop()
     step_s = statistics.mean(dev_s)
     launches = sum(s.meta["kernel_launches"] for s in sols)
+    statuses = sorted({s.status for s in sols})
     # --- e2e through the public API from host buffers
     barrier()
     e2e_s = []
@@ -267,39 +333,46 @@ def run_b200(args, rank, world, local_rank):
         lp2.close()
     barrier()
     e2e_step = statistics.mean(e2e_s)
+    # --- the round-1 criterion (all three <= 1e-4), for continuity
+    flush_l2()
+    kkt = solve(lp, SolverOptions(eps_rel=EPS, eps_res=0.0, time_limit=600.0, max_iters=5_000_000,
+                                  device=dev))
     if dist:
         tt = torch.tensor([step_s, e2e_step], dtype=torch.float64, device=f"cuda:{dev}")
         tdist.all_reduce(tt, op=tdist.ReduceOp.MAX)
         step_s, e2e_step = float(tt[0]), float(tt[1])
-    # --- parity solve (not timed into `value`): residuals to 1e-6, compared
-    # with the reference's optimum for this LP (tests/golden/full_size.json)
+    # --- parity of the timed solves against the reference's optimum for this
+    # LP (tests/golden/full_size.json: collsched's model + HiGHS IPM)
     from paper_2305_13479_b200 import check_lp_schedule, lp_completion_epoch
-    flush_l2()
-    tight = solve(lp, SolverOptions(eps_rel=1e-8, time_limit=600.0, max_iters=5_000_000, device=dev))
-    parity = {"eps_rel": 1e-8, "status": tight.status, "iters": tight.meta["iters"],
-              "device_seconds": tight.meta["device_seconds"], "objective": tight.objective,
-              "completion_epoch": lp_completion_epoch(tight, tol=1e-5)}
-    rep = check_lp_schedule(plan, tight.x, tol=1e-5, device=dev)
-    parity["checker_ok"] = rep.ok
-    gold = golden_for(cfg.K)
+    last = sols[-1]
+    parity = {"criterion": "objective within 1e-4 relative of the reference optimum; relative "
+                           "primal and dual residuals <= 1e-6",
+              "statuses": statuses, "objective": last.objective,
+              "rel_gap": last.meta["rel_gap"], "rel_primal_res": last.meta["rel_primal_res"],
+              "rel_dual_res": last.meta["rel_dual_res"],
+              "completion_epoch": lp_completion_epoch(last, tol=1e-5)}
+    # the answer a user gets from it (synthesize's path): the schedule, its
+    # event-level replay (native simulate) and the integer flow checker on the
+    # flows the events were peeled from
+    from paper_2305_13479_b200.schedule import schedule_with_flows
+    from paper_2305_13479_b200.simulate import simulate
+    t0 = time.perf_counter()
+    sched, xr = schedule_with_flows(last)
+    rep = simulate(sched, t, d)
+    parity["schedule"] = {"events": len(sched.events), "completion_epoch": sched.completion_epoch,
+                          "replay_violations": len(rep.violations),
+                          "replay_completion_epoch": rep.completion_epoch,
+                          "checker_ok": check_lp_schedule(plan, xr, tol=1e-5, device=dev).ok,
+                          "host_seconds": time.perf_counter() - t0, "meta": sched.meta}
     if gold:
-        parity["reference_objective"] = gold["objective"]
-        parity["objective_rel_err"] = abs(tight.objective - gold["objective"]) / abs(gold["objective"])
-        parity["objective_rel_err_at_1e-4"] = abs(sols[-1].objective - gold["objective"]) / abs(gold["objective"])
-        parity["reference_completion_epoch"] = gold["completion_epoch"]
-        parity["reference_highs_seconds"] = gold["highs_ipm_seconds"]
-        # the 1e-4 KKT gap bounds the duality gap, not the distance to the
-        # optimum (primal residual 7e-5 lets the objective overshoot): the
-        # time until the objective itself is within 1e-4 of the reference's
-        for eps in (3e-5, 1e-5, 3e-6, 1e-6):
-            flush_l2()
-            s3 = solve(lp, SolverOptions(eps_rel=eps, time_limit=600.0, max_iters=5_000_000, device=dev))
-            err = abs(s3.objective - gold["objective"]) / abs(gold["objective"])
-            if err <= 1e-4:
-                parity["time_to_objective_within_1e-4_s"] = s3.meta["device_seconds"]
-                parity["objective_within_1e-4_at"] = {"eps_rel": eps, "iters": s3.meta["iters"],
-                                                      "objective_rel_err": err}
-                break
+        errs = [abs(s.objective - gold["objective"]) / abs(gold["objective"]) for s in sols]
+        parity.update({"reference_objective": gold["objective"],
+                       "objective_rel_err_max_over_steps": max(errs),
+                       "reference_completion_epoch": gold["completion_epoch"],
+                       "reference_highs_seconds": gold["highs_ipm_seconds"]})
+        parity["met"] = bool(max(errs) <= 1e-4 and statuses == ["optimal"] and
+                             all(s.meta["rel_primal_res"] <= 1e-6 and s.meta["rel_dual_res"] <= 1e-6
+                                 for s in sols))
     # --- roofline of the dominant fused kernel (live CUDA-event timing):
     # on configs[1] (its ~70 MB iteration working set stays in the 126 MB L2
     # between iterations) and on an HBM-resident LP (8-chassis, 3.9 GB moved
@@ -317,8 +390,8 @@ def run_b200(args, rank, world, local_rank):
         roof["ms_per_iteration"] = sbb["ms_col"] + sbb["ms_row"]
         big.close()
     # --- one LP across all the job's GPUs (strong scaling, informational):
-    # the 8-chassis LP to 1e-4, partitioned by source over the N ranks (one
-    # GPU: the single-device solve), device time max over ranks
+    # the 8-chassis LP to 1e-4 (all three criteria), partitioned by source
+    # over the N ranks (one GPU: the single-device solve), max over ranks
     strong = None
     if not args.no_strong:
         bt, bd, bc = big_workload()
@@ -329,7 +402,8 @@ def run_b200(args, rank, world, local_rank):
                   "device_seconds": out["device_seconds"]}
         else:
             blp = build_from_plan(make_plan(bt, bd, bc), device=dev)
-            bs = solve(blp, SolverOptions(eps_rel=EPS, time_limit=600.0, max_iters=5_000_000, device=dev))
+            bs = solve(blp, SolverOptions(eps_rel=EPS, eps_res=0.0, time_limit=600.0, max_iters=5_000_000,
+                                          device=dev))
             ss = {"status": bs.status, "iters": bs.meta["iters"], "objective": bs.objective,
                   "device_seconds": bs.meta["device_seconds"]}
             blp.close()
@@ -337,14 +411,13 @@ def run_b200(args, rank, world, local_rank):
             tt = torch.tensor([ss["device_seconds"]], dtype=torch.float64, device=f"cuda:{dev}")
             tdist.all_reduce(tt, op=tdist.ReduceOp.MAX)
             ss["device_seconds"] = float(tt[0])
-        strong = {"lp": f"ALLGATHER 8-chassis NDv2 K={BIG_K} (53.2M columns), eps 1e-4",
+        strong = {"lp": f"ALLGATHER 8-chassis NDv2 K={BIG_K} (53.2M columns), eps 1e-4 (all three criteria)",
                   "partition": "by source" if dist else "single GPU", "n_gpus": world,
                   "time_to_1e-4_s": ss["device_seconds"], "iters": ss["iters"],
                   "status": ss["status"], "objective": ss["objective"]}
     if rank != 0:
         return
-    last = sols[-1]
-    cpu = None
+    cpu = uncensored = None
     if world == 1 and not args.no_cpu_baseline:
         from oracle import lp_oracle
         a = lp_oracle.build_lp_arrays(t, d, cfg.tau, cfg.K, d.chunk_size)
@@ -354,20 +427,25 @@ def run_b200(args, rank, world, local_rank):
                "sample": "scipy.optimize.milp/HiGHS on the same configs[1] LP (the call "
                          "collsched.solver.solve makes), capped at 30 s wall; status=" + r["status"],
                "censored": r["status"] != "optimal"}
+        uncensored = reference_uncensored(dev)
     line = {
-        "metric": METRIC, "value": step_s / world, "unit": "s", "n_gpus": world,
+        "metric": METRIC, "value": step_s, "unit": "s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
         "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic",
-        "config": {"workload": WORKLOAD, "K": cfg.K, "eps_rel": EPS, "rows": lp.num_rows,
-                   "cols": lp.num_vars, "nnz": lp.nnz, "per_rank": "one LP solve per step",
-                   "l2": "flushed (256 MiB write) before every step",
-                   "parallelism": f"independent instances x{world}"},
-        "e2e": {"value": e2e_step / world, "unit": "s", "h2d_bytes_per_step": int(h2d),
+        "data": "synthetic", "config": bench_config(cfg),
+        "lp": {"rows": lp.num_rows, "cols": lp.num_vars, "nnz": lp.nnz,
+               "per_rank": "one independent solve of the configs[1] LP per step",
+               "parallelism": f"independent instances x{world}"},
+        "throughput_lps_per_s": world / step_s,
+        "value_kkt_1e-4": {"device_seconds": kkt.meta["device_seconds"], "iters": kkt.meta["iters"],
+                           "status": kkt.status, "objective": kkt.objective,
+                           "criterion": "gap, primal and dual residuals all <= 1e-4 (round 1 headline)"},
+        "e2e": {"value": e2e_step, "unit": "s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h)},
         "roofline": roof or roof_l2,
         "roofline_l2_resident": roof_l2,
         "cpu_baseline": cpu,
+        "reference_uncensored": uncensored,
         "clocks": clk,
         "gpu_launches": int(launches),
         "parity": parity,

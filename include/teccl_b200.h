@@ -5,7 +5,7 @@
  * copy-free time-expanded multi-commodity-flow LP on the CPU:
  *
  *   build_lp_model(t, d, cfg, opts)   pkg/src/collsched/lp.py:22-136
- *   solve(m, opts)  -> scipy HiGHS    pkg/src/collsched/solver.py:87-137
+ *   solve(m, opts)  -> scipy HiGHS    pkg/src/collsched/solver.py:86-143
  *   lp_completion_epoch(sol)          pkg/src/collsched/lp.py:139-153
  *   simulate(sched, t, d, opts)       pkg/src/collsched/simulator.py:58-235
  *
@@ -69,7 +69,7 @@ typedef struct {
   const uint8_t* node_is_switch;  /* [num_nodes] */
   const int32_t* edge_src;        /* [E] node index */
   const int32_t* edge_dst;        /* [E] node index */
-  const int32_t* edge_delta;      /* [E] ceil(alpha/tau), epochs.py:359 */
+  const int32_t* edge_delta;      /* [E] ceil(alpha/tau), epochs.py:58-64 */
   const double* edge_cap;         /* [E*K] chunks/epoch, cap_chunks(), row e*K+k */
   const int32_t* source_node;     /* [S] node index of each source slot */
   const int32_t* pair_source;     /* [P] source slot */
@@ -118,7 +118,7 @@ int teccl_src_connect(teccl_ctx* ctx, teccl_lp* lp, const uint8_t* blobs, int64_
 
 /* Generic LP upload (minimise obj.x s.t. row_lo <= A x <= row_hi,
  * var_lb <= x <= var_ub; +-INFINITY allowed). Replaces the matrix assembly of
- * collsched.solver.solve (solver.py:96-118) for any Model the reference
+ * collsched.solver.solve (solver.py:100-121) for any Model the reference
  * builds. row_ptr has m+1 entries; columns need not be sorted. */
 int teccl_lp_from_csr(teccl_ctx* ctx, int32_t m, int32_t n, int64_t nnz,
                       const int64_t* row_ptr, const int32_t* col, const double* val,
@@ -138,7 +138,7 @@ int teccl_lp_destroy(teccl_lp* lp);
 
 /* ---------------------------------------------------------------------------
  * (2)+(3) Restarted Halpern primal-dual hybrid gradient (PDLP family).
- * Replaces the HiGHS call in collsched.solver.solve (solver.py:119-137) for
+ * Replaces the HiGHS call in collsched.solver.solve (solver.py:128-143) for
  * LPs. Termination: relative duality gap <= eps_rel and relative primal and
  * dual residuals <= min(eps_rel, eps_res) (definitions in DESIGN.md); primal
  * infeasibility is certified on the device (eps_infeas) and reported as

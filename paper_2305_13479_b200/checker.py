@@ -4,7 +4,8 @@ Replays an LP solution of the time-expanded model in fixed-point integer
 units (`quantum` units per chunk): capacity per (edge, epoch), buffer
 causality per (source, node, epoch), switch pass-through, and per-pair
 demand satisfaction, plus the completion epoch. Replaces the reference's
-simulate() (pkg/src/collsched/simulator.py:320-470) for LP schedules.
+simulate() (pkg/src/collsched/simulator.py:58-235) at the flow level for LP
+solutions; the event list itself is replayed by simulate.py.
 """
 
 from __future__ import annotations

@@ -1,6 +1,6 @@
 // C-ABI plumbing: errors, contexts, generic LP upload/export.
 // The generic upload replaces the matrix assembly of the reference solver
-// (pkg/src/collsched/solver.py:96-118) for any Model, so the same PDLP
+// (pkg/src/collsched/solver.py:100-121) for any Model, so the same PDLP
 // kernels serve the reference's own model objects.
 
 #include <algorithm>

@@ -1,7 +1,7 @@
 // (2)+(3) Restarted reflected-Halpern PDHG (PDLP family) on sm_100a.
 //
 // Replaces the CPU LP solve of the reference (pkg/src/collsched/solver.py:
-// 119-137, scipy.optimize.milp -> HiGHS) for the TE-CCL LP.
+// 128-143, scipy.optimize.milp -> HiGHS) for the TE-CCL LP.
 //
 // Formulation. The iteration runs in the ORIGINAL variables with diagonal
 // preconditioners T = tau * D and S = sigma * E, where D = C^2 and E = R^2 come

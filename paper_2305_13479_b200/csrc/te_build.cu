@@ -1004,7 +1004,7 @@ extern "C" int teccl_lp_build_te_part(teccl_ctx* ctx, const teccl_te_desc* desc,
 // ---------------------------------------------------------------------------
 // (4) Exact-integer schedule checker / epoch simulator over an LP solution.
 // Independent of the LP rows: buffers are replayed from the flows alone
-// (reference simulator semantics, simulator.py:381-436, restated for the
+// (reference simulator semantics, simulator.py:119-189, restated for the
 // copy-free per-source flow): a GPU starts with its outgoing demand, loses
 // what it sends and reads, gains what lands delta epochs after a send; a
 // switch must forward exactly what lands, the next epoch.

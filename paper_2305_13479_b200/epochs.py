@@ -1,7 +1,7 @@
 """Epoch arithmetic in exact rationals (reference pkg/src/collsched/epochs.py).
 
 The LP's capacities and link delays are computed here on the host, in the
-same snapped-rational arithmetic as the reference (epochs.py:408-420), so the
+same snapped-rational arithmetic as the reference (epochs.py:107-123), so the
 device builder receives bit-identical float64 capacities and integer delays.
 """
 

@@ -339,7 +339,7 @@ def feasibility_gap(plan: LpPlan, device: int = 0, eps_rel: float = 1e-7,
     and return sum(u) minus its optimum (0 up to solver accuracy iff the
     reference's LP at this horizon is feasible). A phase-1 solve that does not
     converge raises SolverBackendError, like the reference's timed-out
-    horizon probe (solver.py:159-160); its iterate is never a verdict."""
+    horizon probe (solver.py:160-161); its iterate is never a verdict."""
     from dataclasses import replace
     from .errors import SolverBackendError
     from .solver import OPTIMAL, SolverOptions, solve

@@ -11,7 +11,7 @@ eps_res) -- the defaults are north_star's parity bar, gap 1e-4 and residuals
 1e-6 --, "infeasible" when the device found a Farkas certificate
 (teccl_pdlp_opts.eps_infeas; x is None, like the reference's), "timeout" on
 the iteration / time cap. A numerical failure raises SolverBackendError, as
-the reference does for an unexpected HiGHS status (solver.py:134-135).
+the reference does for an unexpected HiGHS status (solver.py:136-138).
 """
 
 from __future__ import annotations
@@ -100,7 +100,7 @@ def pdlp_options(opts: SolverOptions, verbose: int = 0) -> nat.PdlpOpts:
 
 def _upload_generic(m, device: int) -> DeviceLP:
     """Reference-style Model (num_vars, kinds, lb, ub, rows, objective) ->
-    device LP, minimisation form c = -objective (solver.py:96-118)."""
+    device LP, minimisation form c = -objective (solver.py:100-121)."""
     ctx = nat.Context.get(device)
     n = m.num_vars
     c = np.zeros(n)

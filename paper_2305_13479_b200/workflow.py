@@ -62,7 +62,7 @@ def feasible_horizon(t: Topology, d: Demand, cfg: EpochConfig, opts: ModelOption
                      sopts: SolverOptions | None = None) -> tuple:
     """(K, solution) for the smallest K = k0 * 2^j whose LP is feasible. Each
     probe is one solve: "infeasible" (the device certificate) doubles K, a
-    timed-out probe raises like the reference's (solver.py:159-160)."""
+    timed-out probe raises like the reference's (solver.py:160-161)."""
     sopts = sopts or SolverOptions(device=device)
     K = max(1, k0)
     while K <= k_max:
