@@ -185,6 +185,13 @@ typedef struct {
                                  this fraction of its terms' magnitude; 0 disables (1e-6).
                                  Single-device solves only */
   int32_t infeas_every;       /* checks between certificate evaluations (4) */
+  int32_t persist;            /* 1: run each chunk of iterations as one persistent cooperative
+                                 kernel (dense state in shared memory, grid barriers between
+                                 half-steps) when the LP is on the stored operator and every
+                                 block's share fits in shared memory -- L2-resident LPs such as
+                                 configs[1]; same arithmetic per entry, partial sums of the
+                                 restart metrics in another order) (0: measured slower) */
+  double omega_bias;          /* multiplies the primal-weight target dy/dx at restarts (1.0) */
 } teccl_pdlp_opts;
 
 typedef struct {

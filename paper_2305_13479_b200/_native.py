@@ -56,7 +56,8 @@ class PdlpOpts(C.Structure):
         ("omega_ki", C.c_double), ("omega_kd", C.c_double), ("col_pipeline", C.c_int32),
         ("matrix_free", C.c_int32), ("pdl", C.c_int32),
         ("fused_halo", C.c_int32), ("eps_res", C.c_double), ("eps_infeas", C.c_double),
-        ("infeas_every", C.c_int32),
+        ("infeas_every", C.c_int32), ("persist", C.c_int32),
+        ("omega_bias", C.c_double),
     ]
 
 

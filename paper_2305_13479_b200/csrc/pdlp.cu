@@ -71,6 +71,7 @@ constexpr int kNQ = 15;          // partial quantities per check (9 KKT + 6 infe
 constexpr int kSlice = 32;
 constexpr int kSegTPW = TECCL_SEG_TPW;
 constexpr int kTile = kThreads;  // rows (columns) per block of the step kernels
+constexpr int kPersistThreads = 1024;  // threads per block of the persistent chunk kernel
 // auto operator (matrix_free = 1): matrix-free kernels from this many columns
 // up (configs[1], 0.97M columns, runs L2-resident on the stored SELL kernels)
 constexpr int64_t kAutoMatrixFreeCols = 3000000;
@@ -93,6 +94,7 @@ struct PdlpState {
   double eps;
   double r0, rprev, last_r;
   double rs_suff, rs_nec, rs_art, theta, ki, kd, e_int, e_prev;
+  double bias;               // log of the primal-weight target bias (omega_bias)
   long long k_inner, total;
   int have_r0, restart, done, restarts, chunk_len, pad;
   double rel_p, rel_d, gap, pobj, dobj;
@@ -662,6 +664,182 @@ __global__ void __launch_bounds__(kThreads, TECCL_ROW_MINB) row_step_kernel(int3
 }
 
 // ---------------------------------------------------------------------------
+// Persistent chunk kernel (LPs whose iteration is L2-resident, on the stored
+// SELL operator: configs[1]). One cooperative launch runs a whole chunk of
+// `check_every` iterations. Block b owns a contiguous, slice-aligned range of
+// columns and one of rows and keeps their dense state -- x, x0, D and the
+// bound class of its columns; y, y0, E and the class of its rows, plus both
+// bound dictionaries -- in shared memory for the whole chunk, so an iteration
+// moves only the index streams and the gathered vectors (y for the column
+// half-step, xbar for the row half-step) through L2. The gathers use
+// ld.global.cg: other blocks wrote those vectors earlier in this launch. The
+// half-steps are separated by grid barriers instead of kernel boundaries.
+// Same arithmetic, in the same order, as col_pipe_kernel / row_step_kernel.
+struct Persist {
+  int cpb, rpb;            // columns / rows per block (multiples of the SELL slice)
+  int ncd, nrd;            // bound-dictionary entries (DICT)
+  int chunk;               // iterations per launch (<= kLamTab)
+  unsigned int* bar;       // grid-barrier counter, zeroed before each launch
+  size_t smem;             // dynamic shared memory per block
+};
+
+__device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int& target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    target += gridDim.x;
+    __threadfence();  // this block's stores (xbar / y) before its arrival
+    atomicAdd(bar, 1u);
+    unsigned int v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+    } while ((int)(v - target) < 0);
+  }
+  __syncthreads();
+}
+
+// sell_dot over a vector written by other blocks of this launch (L2, not L1)
+template <bool UNIT, int G>
+__device__ __forceinline__ double sell_dot_cg(const SellView& S, uint32_t r, const double* __restrict__ v) {
+  const uint32_t s = r >> 5;
+  const int w = __ldg(S.width + s);
+  const uint32_t* ip = S.idx + __ldg(S.off + s) + (r & 31);
+  const double* vp = UNIT ? nullptr : S.val + (ip - S.idx);
+  double acc = 0.0;
+  for (int q = 0; q < w; q += G) {
+    uint32_t t[G];
+#pragma unroll
+    for (int u = 0; u < G; ++u) t[u] = (q + u < w) ? __ldg(ip + (q + u) * kSlice) : 0u;
+#pragma unroll
+    for (int u = 0; u < G; ++u) {
+      if (q + u < w) {
+        if (UNIT) {
+          const double xv = __ldcg(v + (t[u] & kIdxMask));
+          acc += __hiloint2double(__double2hiint(xv) ^ (int)(t[u] & kSignBit), __double2loint(xv));
+        } else {
+          acc += __ldg(vp + (q + u) * kSlice) * __ldcg(v + t[u]);
+        }
+      }
+    }
+  }
+  return acc;
+}
+
+template <bool UNIT, bool DICT>
+__global__ void __launch_bounds__(kPersistThreads, 1) chunk_persist_kernel(int32_t n, int32_t m, SellView SC,
+                                                                           SellView SR, Vecs Vc, Vecs Vr,
+                                                                           Persist P) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ double sh[32];
+  const PdlpState* st = Vc.st;
+  if (st->done) return;  // read before any barrier: every block takes the same branch
+  const double tau = st->tau, sigma = st->sigma, refl = st->refl;
+  const int c0 = blockIdx.x * P.cpb, nc = max(0, min(P.cpb, n - c0));
+  const int r0 = blockIdx.x * P.rpb, nr = max(0, min(P.rpb, m - r0));
+  // shared-memory layout: doubles, then floats, then uint16 codes
+  double* xs = (double*)smem;
+  double* ys = xs + P.cpb;
+  double* cdict = ys + P.rpb;                 // [3 * ncd]
+  double* rdict = cdict + 3 * P.ncd;          // [2 * nrd]
+  double* lam = rdict + 2 * P.nrd;            // [chunk]
+  float* x0s = (float*)(lam + P.chunk);
+  float* Ds = x0s + P.cpb;
+  float* y0s = Ds + P.cpb;
+  float* Es = y0s + P.rpb;
+  uint16_t* ccode = (uint16_t*)(Es + P.rpb);
+  uint16_t* rcode = ccode + P.cpb;
+  for (int q = threadIdx.x; q < nc; q += blockDim.x) {
+    const int64_t j = c0 + q;
+    xs[q] = Vc.x[j];
+    x0s[q] = Vc.x0[j];
+    Ds[q] = Vc.D[j];
+    if (DICT) ccode[q] = Vc.col.code[j];
+  }
+  for (int q = threadIdx.x; q < nr; q += blockDim.x) {
+    const int64_t i = r0 + q;
+    ys[q] = Vr.y[i];
+    y0s[q] = Vr.y0[i];
+    Es[q] = Vr.E[i];
+    if (DICT) rcode[q] = Vr.row.code[i];
+  }
+  if (DICT) {
+    for (int q = threadIdx.x; q < 3 * P.ncd; q += blockDim.x) cdict[q] = Vc.col.dict[q];
+    for (int q = threadIdx.x; q < 2 * P.nrd; q += blockDim.x) rdict[q] = Vr.row.dict[q];
+  }
+  for (int q = threadIdx.x; q < P.chunk; q += blockDim.x) lam[q] = st->lam_tab[q];
+  __syncthreads();
+  unsigned int target = 0;
+  for (int it = 0; it < P.chunk; ++it) {
+    const bool check = (it == P.chunk - 1);
+    const double l = lam[it];
+    // --- primal half-step over this block's columns: A^T y, step, projection,
+    // reflection, Halpern average (col_pipe_kernel)
+    double dx = 0.0, dx0 = 0.0;
+    for (int q = threadIdx.x; q < nc; q += blockDim.x) {
+      const int64_t j = c0 + q;
+      double lb, ub, cj;
+      if (DICT) {
+        const double* e = cdict + 3 * ccode[q];
+        lb = e[0]; ub = e[1]; cj = e[2];
+      } else {
+        lb = __ldg(Vc.col.a + j); ub = __ldg(Vc.col.b + j); cj = __ldg(Vc.col.c + j);
+      }
+      const double s = sell_dot_cg<UNIT, 4>(SC, (uint32_t)j, Vc.y);
+      const double xj = xs[q], x0 = (double)x0s[q], Dj = (double)Ds[q];
+      const double xt = clampd(xj - tau * Dj * (cj - s), lb, ub);
+      Vc.xbar[j] = 2.0 * xt - xj;
+      xs[q] = l * ((1.0 + refl) * xt - refl * xj) + (1.0 - l) * x0;
+      if (check) {
+        Vc.xt[j] = xt;
+        const double w = 1.0 / Dj;
+        dx += (xt - xj) * (xt - xj) * w;
+        dx0 += (xt - x0) * (xt - x0) * w;
+      }
+    }
+    if (check) {
+      double a = block_sum(dx, sh);
+      if (threadIdx.x == 0) Vc.part[Q_DX * Vc.pstride + blockIdx.x] = a;
+      a = block_sum(dx0, sh);
+      if (threadIdx.x == 0) Vc.part[Q_DX0 * Vc.pstride + blockIdx.x] = a;
+    }
+    grid_barrier(P.bar, target);
+    // --- dual half-step over this block's rows: A xbar, step, projection,
+    // Halpern average (row_step_kernel)
+    double dy = 0.0, dy0 = 0.0;
+    for (int q = threadIdx.x; q < nr; q += blockDim.x) {
+      const int64_t i = r0 + q;
+      double lo, hi;
+      if (DICT) {
+        const double* e = rdict + 2 * rcode[q];
+        lo = e[0]; hi = e[1];
+      } else {
+        lo = __ldg(Vr.row.a + i); hi = __ldg(Vr.row.b + i);
+      }
+      const double s = sell_dot_cg<UNIT, TECCL_ROW_G>(SR, (uint32_t)i, Vr.xbar);
+      const double yi = ys[q], y0 = (double)y0s[q], Ei = (double)Es[q];
+      const double se = sigma * Ei;
+      const double yt = dual_step(yi, s, se, lo, hi);
+      const double yn = l * ((1.0 + refl) * yt - refl * yi) + (1.0 - l) * y0;
+      ys[q] = yn;
+      Vr.y[i] = yn;
+      if (check) {
+        Vr.yt[i] = yt;
+        const double w = 1.0 / Ei;
+        dy += (yt - yi) * (yt - yi) * w;
+        dy0 += (yt - y0) * (yt - y0) * w;
+      }
+    }
+    if (check) {
+      double a = block_sum(dy, sh);
+      if (threadIdx.x == 0) Vr.part[Q_DY * Vr.pstride + blockIdx.x] = a;
+      a = block_sum(dy0, sh);
+      if (threadIdx.x == 0) Vr.part[Q_DY0 * Vr.pstride + blockIdx.x] = a;
+    }
+    if (!check) grid_barrier(P.bar, target);  // the launch boundary orders the last one
+  }
+  for (int q = threadIdx.x; q < nc; q += blockDim.x) Vc.x[c0 + q] = xs[q];
+}
+
+// ---------------------------------------------------------------------------
 // Matrix-free half-steps for LPs built by teccl_lp_build_te: the same
 // updates as col_step / row_step, with A^T y and A x evaluated from the
 // topology tables (te_gen.cuh) and the bounds/costs computed in place. No
@@ -970,6 +1148,38 @@ __global__ void __launch_bounds__(kThreads) col_seg_kernel(TeOp op, Vecs V, int 
   }
 }
 
+// TECCL_SEG_TMA: each warp stages its task's rows of y, y0 and E in shared
+// memory with three 1-D bulk copies (cp.async.bulk, completion on a per-warp
+// mbarrier) issued in the prologue, before griddepcontrol.wait -- they are
+// final two launches back -- so they stream while the warp gathers x-bar,
+// and the epilogue reads shared memory instead of issuing dependent L2 loads
+// (it used to L2-prefetch them and load them after the gathers).
+#ifndef TECCL_SEG_TMA
+#define TECCL_SEG_TMA 1
+#endif
+
+struct alignas(16) SegStage {  // 16-byte multiple: every warp's stage is a bulk-copy destination
+  double y[kSegTask + 2];   // [first & ~1, round_up_even(first + cnt))
+  float y0[kSegTask + 4];   // [first & ~3, round_up_4(first + cnt))
+  float E[kSegTask + 4];
+  unsigned long long bar;
+};
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               :: "r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+                 : "=r"(done) : "r"(smem_addr(bar)), "r"(parity) : "memory");
+  }
+}
+
 template <bool CHECK>
 __global__ void __launch_bounds__(kThreads, TECCL_SEG_MINB) row_seg_kernel(TeOp op, Vecs V, int j_in_chunk) {
   __shared__ double sh[32];
@@ -978,6 +1188,25 @@ __global__ void __launch_bounds__(kThreads, TECCL_SEG_MINB) row_seg_kernel(TeOp 
 #pragma unroll
   for (int t = 0; t < kSegTPW; ++t)
     tks[t] = (w0 + t < op.n_rtask) ? __ldg(op.rtask + w0 + t) : make_int4(0, 0, 0, 0);
+#if TECCL_SEG_TMA
+  static_assert(kSegTPW == 1, "TMA staging is per warp task");
+  __shared__ __align__(16) SegStage stage[kThreads / 32];
+  SegStage& sg = stage[threadIdx.x >> 5];
+  const int cnt0 = seg_count(tks[0]);
+  const uint32_t f0 = (uint32_t)tks[0].z;
+  const uint32_t a2 = f0 & ~1u, a4 = f0 & ~3u;
+  if (lane == 0 && cnt0 > 0) {
+    const uint32_t by = ((f0 + cnt0 + 1u) & ~1u) - a2, b4 = ((f0 + cnt0 + 3u) & ~3u) - a4;
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(smem_addr(&sg.bar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                 :: "r"(smem_addr(&sg.bar)), "r"(8u * by + 8u * b4) : "memory");
+    bulk_g2s(sg.y, V.y + a2, 8u * by, &sg.bar);
+    bulk_g2s(sg.y0, V.y0 + a4, 4u * b4, &sg.bar);
+    bulk_g2s(sg.E, V.E + a4, 4u * b4, &sg.bar);
+  }
+  __syncwarp();
+#else
   // the dense operands are only prefetched into L2 here and loaded after the
   // gathers: held in registers across seg_rows they were spilled at 40
   // registers, and the spill store waited for the HBM load before any
@@ -990,6 +1219,7 @@ __global__ void __launch_bounds__(kThreads, TECCL_SEG_MINB) row_seg_kernel(TeOp 
       prefetch_l2(V.y + r);
       if ((lane & 1) == 0) { prefetch_l2(V.y0 + r); prefetch_l2(V.E + r); }
     }
+#endif
   pdl_wait();
   pdl_trigger();
   const PdlpState* st = V.st;
@@ -1001,15 +1231,25 @@ __global__ void __launch_bounds__(kThreads, TECCL_SEG_MINB) row_seg_kernel(TeOp 
     const uint32_t first = (uint32_t)tk.z;
     double s[kSegPerLane], lo[kSegPerLane], hi[kSegPerLane];
     seg_rows(op, tk, lane, V.xbar, s, lo, hi);
+#if TECCL_SEG_TMA
+    if (cnt > 0) mbar_wait(&sg.bar, 0);  // the staged rows (long since landed, normally);
+                                         // also: no bulk copy may outlive the block
+#endif
     if (st->done) return;
     const double sigma = st->sigma, refl = st->refl;
     double yi[kSegPerLane], y0[kSegPerLane], Ei[kSegPerLane];
 #pragma unroll
     for (int h = 0; h < kSegPerLane; ++h) {
       const uint32_t r = first + (uint32_t)max(0, min(lane + 32 * h, cnt - 1));
+#if TECCL_SEG_TMA
+      yi[h] = sg.y[r - a2];
+      y0[h] = (double)sg.y0[r - a4];
+      Ei[h] = (double)sg.E[r - a4];
+#else
       yi[h] = V.y[r];
       y0[h] = (double)V.y0[r];
       Ei[h] = (double)V.E[r];
+#endif
     }
     const double lam = st->lam_tab[j_in_chunk];  // chunks are at most kLamTab iterations
 #pragma unroll
@@ -1459,7 +1699,7 @@ __device__ void control_decide(Vecs V) {
     if (dxr > 1e-10 && dyr > 1e-10) {
       // PID on the log primal-weight error e = log(dy/dx) - log(w); with
       // ki = kd = 0 this is PDLP's exponential smoothing with weight theta
-      const double e = log(dyr / dxr) - log(w);
+      const double e = log(dyr / dxr) + st->bias - log(w);
       st->e_int += e;
       const double de = e - st->e_prev;
       st->e_prev = e;
@@ -1790,6 +2030,7 @@ struct Workspace {
   // dual iterate and the ray candidate (pad slot [m] = 0 for SELL gathers)
   double *ubI = nullptr, *loI = nullptr, *hiI = nullptr, *yprev = nullptr, *dv = nullptr;
   PdlpState* dst = nullptr;
+  unsigned int* bar = nullptr;    // grid-barrier counter of the persistent chunk kernel
   int64_t pstride = 0;
   cudaGraphExec_t gexec = nullptr;
   int graph_chunk = 0;  // key of the captured graph: chunk length and kernel variant
@@ -1995,11 +2236,31 @@ struct Infeas {
   double *yprev = nullptr, *dv = nullptr;
 };
 
+// One cooperative launch of chunk_persist_kernel (a memset node resets the
+// grid-barrier counter first).
+template <bool UNIT, bool DICT>
+void launch_persist(cudaStream_t st, const teccl_lp* lp, const Vecs& Vc, const Vecs& Vr, const Persist& P) {
+  cudaMemsetAsync(P.bar, 0, sizeof(unsigned int), st);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(kSMs);
+  cfg.blockDim = dim3(kPersistThreads);
+  cfg.dynamicSmemBytes = P.smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, chunk_persist_kernel<UNIT, DICT>, (int32_t)lp->n, (int32_t)lp->m, col_view(lp),
+                     row_view(lp), Vc, Vr, P);
+}
+
 template <bool UNIT, bool DICT>
 void enqueue_chunk(int chunk, cudaStream_t st, const teccl_lp* lp, const TeOp* te, const EmOp* em, const Vecs& Vc, const Vecs& Vr,
-                   Exchange& X, double* y_w, double* yt_w, const Infeas& IF) {
+                   Exchange& X, double* y_w, double* yt_w, const Infeas& IF, const Persist* PL) {
   const int64_t nrw = gather_rows(lp), orr = own_row_off(lp);
-  for (int j = 0; j < chunk; ++j) {
+  if (PL) launch_persist<UNIT, DICT>(st, lp, Vc, Vr, *PL);
+  for (int j = 0; !PL && j < chunk; ++j) {
     const bool check = (j == chunk - 1);
     if (check) launch_col<UNIT, DICT, true>(st, lp, te, em, Vc, j);
     else launch_col<UNIT, DICT, false>(st, lp, te, em, Vc, j);
@@ -2151,8 +2412,9 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
     if (sp) W.pstride = std::max<int64_t>(W.pstride, src_blk_off + src_nb_fin);
     W.rstat = W.alloc<double>(m); W.cstat = W.alloc<double>(n);
     // pad slot [n] / [m]: the two-column kernels load pairs unconditionally
-    W.D = W.alloc<float>(n + 1); W.E = W.alloc<float>(m + 1);
-    W.x0 = W.alloc<float>(n + 1); W.y0 = W.alloc<float>(m + 1);
+    // E, y0: +4 so the row kernels' 16-byte bulk copies may round a range up
+    W.D = W.alloc<float>(n + 1); W.E = W.alloc<float>(m + 4);
+    W.x0 = W.alloc<float>(n + 1); W.y0 = W.alloc<float>(m + 4);
     W.x = W.alloc<double>(n + 1);
     if (!ds) {  // single device: the gather windows are the owned vectors
       W.R = W.alloc<double>(m + 1); W.C = W.alloc<double>(n + 1);
@@ -2375,6 +2637,7 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
   hs.theta = o->omega_theta;
   hs.ki = o->omega_ki;
   hs.kd = o->omega_kd;
+  hs.bias = o->omega_bias > 0.0 ? log(o->omega_bias) : 0.0;
   const int chunk = std::min(o->check_every > 0 ? o->check_every : 64, kLamTab);
   hs.chunk_len = chunk;
   for (int j = 0; j < kLamTab; ++j) hs.lam_tab[j] = (j + 1.0) / (j + 2.0);
@@ -2425,6 +2688,31 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
       v->seg = 0;
     }
   }
+  // --- persistent chunk kernel: stored SELL operator on one device, when every
+  // block's dense state fits in shared memory (L2-resident LPs: configs[1])
+  Persist PP{};
+  const Persist* PL = nullptr;
+  if (o->persist && !te && !em && !ds && !sp && !sb && chunk <= kLamTab) {
+    PP.cpb = (int)((((int64_t)n + kSMs - 1) / kSMs + kSlice - 1) / kSlice * kSlice);
+    PP.rpb = (int)((((int64_t)m + kSMs - 1) / kSMs + kSlice - 1) / kSlice * kSlice);
+    PP.ncd = DICT ? lp->n_col_dict : 0;
+    PP.nrd = DICT ? lp->n_row_dict : 0;
+    PP.chunk = chunk;
+    PP.smem = sizeof(double) * ((size_t)PP.cpb + PP.rpb + 3 * PP.ncd + 2 * PP.nrd + chunk) +
+              sizeof(float) * 2 * ((size_t)PP.cpb + PP.rpb) + (DICT ? sizeof(uint16_t) * ((size_t)PP.cpb + PP.rpb) : 0);
+    int occ = 0;
+    if (PP.smem <= (size_t)200 * 1024 &&
+        cudaFuncSetAttribute(chunk_persist_kernel<UNIT, DICT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)PP.smem) == cudaSuccess &&
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, chunk_persist_kernel<UNIT, DICT>, kPersistThreads,
+                                                      PP.smem) == cudaSuccess &&
+        occ >= 1) {
+      if (!W.bar) W.bar = W.alloc<unsigned int>(1);
+      PP.bar = W.bar;
+      if (PP.bar) PL = &PP;
+    }
+    cudaGetLastError();  // a refused attribute only means: no persistent kernel
+  }
   init_iterates_kernel<<<gr, kThreads, 0, st>>>(n, m, Vi, o->warm_start, x_dev, y_dev);
   nl += 1;
   if (o->warm_start) X.halo(st, {A_Y, A_YT});
@@ -2473,7 +2761,7 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
   }
 
   // --- chunk graph (captured once per LP and chunk length)
-  const int graph_key = chunk * 512 + (o->col_pipeline ? 1 : 0) + (te || em ? 2 : 0) + (o->pdl ? 4 : 0) + 8 * V.seg + 32 * o->fused_halo + (sp ? 128 : 0) + (IF.on ? 256 : 0);
+  const int graph_key = chunk * 1024 + (o->col_pipeline ? 1 : 0) + (te || em ? 2 : 0) + (o->pdl ? 4 : 0) + 8 * V.seg + 32 * o->fused_halo + (sp ? 128 : 0) + (IF.on ? 256 : 0) + (PL ? 512 : 0);
   if (o->use_graphs && W.gexec && W.graph_chunk != graph_key) {
     cudaGraphExecDestroy(W.gexec);
     W.gexec = nullptr;
@@ -2491,7 +2779,7 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
       enqueue_chunk_src<UNIT, DICT>(chunk, cap, lp, te, sp, Vc, Vr, src_nb_col, src_nb_own, src_nb_fin,
                                     src_blk_off, y_w, yt_w);
     else
-      enqueue_chunk<UNIT, DICT>(chunk, cap, lp, te, em, Vc, Vr, X, y_w, yt_w, IF);
+      enqueue_chunk<UNIT, DICT>(chunk, cap, lp, te, em, Vc, Vr, X, y_w, yt_w, IF, PL);
     TECCL_CUDA(cudaStreamEndCapture(cap, &g));
     TECCL_CUDA(cudaGraphInstantiate(&W.gexec, g, 0));
     TECCL_CUDA(cudaGraphDestroy(g));
@@ -2499,7 +2787,7 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
     W.graph_chunk = graph_key;
   }
   cudaGraphExec_t gexec = o->use_graphs ? W.gexec : nullptr;
-  per_chunk = sp ? 4LL * chunk + 7 : 2LL * chunk + 6 + (IF.on ? 2 : 0) + (X.active() ? (Vc.push.n || Vr.push.n ? (Vc.wait.npeer ? 2LL : 2LL * chunk + 2) : 4LL * chunk + 1) : 0);
+  per_chunk = sp ? 4LL * chunk + 7 : (PL ? 1LL : 2LL * chunk) + 6 + (IF.on ? 2 : 0) + (X.active() ? (Vc.push.n || Vr.push.n ? (Vc.wait.npeer ? 2LL : 2LL * chunk + 2) : 4LL * chunk + 1) : 0);
   mark("graph");
 
   // --- iterate: chunks queued `lookahead` deep; the device stops itself
@@ -2532,7 +2820,7 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
           enqueue_chunk_src<UNIT, DICT>(chunk, st, lp, te, sp, Vc, Vr, src_nb_col, src_nb_own, src_nb_fin,
                                         src_blk_off, y_w, yt_w);
         else
-          enqueue_chunk<UNIT, DICT>(chunk, st, lp, te, em, Vc, Vr, X, y_w, yt_w, IF);
+          enqueue_chunk<UNIT, DICT>(chunk, st, lp, te, em, Vc, Vr, X, y_w, yt_w, IF, PL);
       }
       TECCL_CHECK_LAUNCH();
       const int slot = (int)(launched % look);
@@ -2635,6 +2923,8 @@ extern "C" void teccl_pdlp_default_opts(teccl_pdlp_opts* o) {
   o->eps_res = 1e-6;
   o->eps_infeas = 1e-6;
   o->infeas_every = 4;
+  o->omega_bias = 1.0;
+  o->persist = 0;  // measured slower than the two-kernel iteration (profiles/r02_d_persist.md)
 }
 
 extern "C" int teccl_pdlp_solve_dev(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* opts,

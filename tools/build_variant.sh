@@ -12,7 +12,7 @@ mkdir -p ../../build_variants
 NV="/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O3 --expt-relaxed-constexpr"
 srcs=${SRCS:-pdlp.cu}
 objs=""
-for f in capi.cu te_build.cu pdlp.cu sell.cu schedule.cu; do
+for f in capi.cu te_build.cu pdlp.cu sell.cu schedule.cu simulate.cu; do
   if [[ " $srcs " == *" $f "* ]]; then
     $NV "$@" -c $f -o ../../build_variants/${f%.cu}_$name.o
     objs="$objs ../../build_variants/${f%.cu}_$name.o"
