@@ -397,7 +397,7 @@ def run_b200(args, rank, world, local_rank):
         bt, bd, bc = big_workload()
         if dist:
             from paper_2305_13479_b200.dist import solve_source_partitioned
-            out = solve_source_partitioned(bt, bd, bc, eps_rel=EPS, device=dev)
+            out = solve_source_partitioned(bt, bd, bc, eps_rel=EPS, eps_res=0.0, device=dev)
             ss = {"status": out["status"], "iters": out["iters"], "objective": out["objective"],
                   "device_seconds": out["device_seconds"]}
         else:
@@ -437,6 +437,7 @@ def run_b200(args, rank, world, local_rank):
                "per_rank": "one independent solve of the configs[1] LP per step",
                "parallelism": f"independent instances x{world}"},
         "throughput_lps_per_s": world / step_s,
+        "censored": statuses != ["optimal"],  # a timed solve that stopped on a cap is not a time-to-answer
         "value_kkt_1e-4": {"device_seconds": kkt.meta["device_seconds"], "iters": kkt.meta["iters"],
                            "status": kkt.status, "objective": kkt.objective,
                            "criterion": "gap, primal and dual residuals all <= 1e-4 (round 1 headline)"},

@@ -117,11 +117,13 @@ def partition_epochs(K: int, world: int) -> list[tuple[int, int]]:
 
 
 def solve_partitioned(t, d, cfg, opts=None, eps_rel: float = 1e-4, max_iters: int = 5_000_000,
+                      eps_res: float = 1e-6,
                       device: int | None = None, group=None, gather: bool = False,
                       pdlp: dict | None = None) -> dict:
     """Collective call: every rank of the process group solves its epoch
     block; returns the (identical) global status/objective on every rank and,
-    with gather=True, the full solution in reference column order."""
+    with gather=True, the full solution in reference column order on rank 0
+    (gather="all": on every rank)."""
     import torch
     import torch.distributed as dist
     from .solver import SolverOptions, pdlp_options
@@ -134,7 +136,7 @@ def solve_partitioned(t, d, cfg, opts=None, eps_rel: float = 1e-4, max_iters: in
         from .lp import build_from_plan
         from .solver import solve
         lp = build_from_plan(plan, device)
-        sol = solve(lp, SolverOptions(eps_rel=eps_rel, max_iters=max_iters, device=device,
+        sol = solve(lp, SolverOptions(eps_rel=eps_rel, eps_res=eps_res, max_iters=max_iters, device=device,
                                       pdlp=pdlp or {}))
         out = {"status": sol.status, "objective": sol.objective, "iters": sol.meta["iters"],
                "restarts": sol.meta["restarts"], "rel_gap": sol.meta["rel_gap"],
@@ -159,7 +161,7 @@ def solve_partitioned(t, d, cfg, opts=None, eps_rel: float = 1e-4, max_iters: in
     x = np.empty(max(1, n_own))
     y = np.empty(max(1, m_own))
     res = nat.PdlpResult()
-    o = pdlp_options(SolverOptions(eps_rel=eps_rel, max_iters=max_iters, device=device,
+    o = pdlp_options(SolverOptions(eps_rel=eps_rel, eps_res=eps_res, max_iters=max_iters, device=device,
                                    pdlp=pdlp or {}))
     nat.check(part.ctx.lib.teccl_pdlp_solve(part.ctx.handle, part.handle, C.byref(o),
                                             nat.ptr(x, C.c_double), nat.ptr(y, C.c_double),
@@ -170,14 +172,18 @@ def solve_partitioned(t, d, cfg, opts=None, eps_rel: float = 1e-4, max_iters: in
            "rel_dual_res": res.rel_dual_res, "device_seconds": res.solve_seconds,
            "kernel_launches": int(res.spmv_launches), "world": world, "rank": rank,
            "info": part.info}
-    if gather:
+    if gather:  # the full solution on rank 0 (gather="all": on every rank)
+        piece = (part.info["own_c0"], part.info["own_c1"], x[:n_own])
         pieces = [None] * world
-        dist.all_gather_object(pieces, (part.info["own_c0"], part.info["own_c1"], x[:n_own]),
-                               group=group)
-        full = np.empty(plan.num_vars)
-        for c0, c1, xs in pieces:
-            full[em_to_ref_cols(plan, c0, c1)] = xs
-        out["x"] = full
+        if gather == "all":
+            dist.all_gather_object(pieces, piece, group=group)
+        else:
+            dist.gather_object(piece, pieces if rank == 0 else None, dst=0, group=group)
+        if gather == "all" or rank == 0:
+            full = np.empty(plan.num_vars)
+            for c0, c1, xs in pieces:
+                full[em_to_ref_cols(plan, c0, c1)] = xs
+            out["x"] = full
         out["plan"] = plan
     part.close()
     return out
@@ -187,6 +193,7 @@ SRC_INFO_KEYS = ("s0", "s1", "p0", "p1", "c0", "c1", "q0", "q1")
 
 
 def solve_source_partitioned(t, d, cfg, opts=None, eps_rel: float = 1e-4, max_iters: int = 5_000_000,
+                             eps_res: float = 1e-6,
                              device: int | None = None, group=None, gather: bool = False,
                              pdlp: dict | None = None) -> dict:
     """Collective call: ONE LP across the ranks of the group, partitioned by
@@ -222,7 +229,7 @@ def solve_source_partitioned(t, d, cfg, opts=None, eps_rel: float = 1e-4, max_it
     x = np.empty(plan.num_vars)
     y = np.empty(plan.num_rows)
     res = nat.PdlpResult()
-    o = pdlp_options(SolverOptions(eps_rel=eps_rel, max_iters=max_iters, device=device,
+    o = pdlp_options(SolverOptions(eps_rel=eps_rel, eps_res=eps_res, max_iters=max_iters, device=device,
                                    pdlp=pdlp or {}))
     nat.check(lp.ctx.lib.teccl_pdlp_solve(lp.ctx.handle, lp.handle, C.byref(o),
                                           nat.ptr(x, C.c_double), nat.ptr(y, C.c_double),
