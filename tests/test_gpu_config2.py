@@ -58,7 +58,7 @@ def test_config2_four_chassis_certified_optimum():
     t, d, cfg = _cfg(4, 1933)
     plan = make_plan(t, d, cfg)
     lp = build_from_plan(plan)
-    assert lp.num_vars == 43_318_272
+    assert lp.num_vars == 43_303_296
     sol = solve(lp, SolverOptions(eps_rel=1e-8, time_limit=600, max_iters=5_000_000))
     assert sol.status == "optimal"
     # duality-gap certificate: primal and dual objectives agree to 1e-8
