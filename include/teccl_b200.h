@@ -192,6 +192,8 @@ typedef struct {
                                  configs[1]; same arithmetic per entry, partial sums of the
                                  restart metrics in another order) (0: measured slower) */
   double omega_bias;          /* multiplies the primal-weight target dy/dx at restarts (1.0) */
+  double step_safety;         /* eta = step_safety / (power-iteration estimate of
+                                 ||E^1/2 A D^1/2||_2), in (0, 1) (0.998) */
 } teccl_pdlp_opts;
 
 typedef struct {

@@ -57,7 +57,7 @@ class PdlpOpts(C.Structure):
         ("matrix_free", C.c_int32), ("pdl", C.c_int32),
         ("fused_halo", C.c_int32), ("eps_res", C.c_double), ("eps_infeas", C.c_double),
         ("infeas_every", C.c_int32), ("persist", C.c_int32),
-        ("omega_bias", C.c_double),
+        ("omega_bias", C.c_double), ("step_safety", C.c_double),
     ]
 
 

@@ -2619,7 +2619,9 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
   TECCL_CUDA(cudaMemsetAsync(part, 0, sizeof(double) * kNQ * pstride, st));
   // --- state: omega in original space = scaled weight * gamma / beta
   PdlpState hs{};
-  hs.eta = 0.998 / sigma_max;
+  hs.eta = (o->step_safety > 0.0 && o->step_safety < 1.0 ? o->step_safety : 0.998) / sigma_max;
+  if (o->verbose > 0)
+    fprintf(stderr, "[teccl pdlp r%d] power iteration: ||E^1/2 A D^1/2|| ~ %.9g, eta %.6g\n", rank, sigma_max, hs.eta);
   hs.omega = omega_s * gamma / beta * (o->omega_scale > 0.0 ? o->omega_scale : 1.0);
   hs.tau = hs.eta / hs.omega;
   hs.sigma = hs.eta * hs.omega;
@@ -2924,6 +2926,7 @@ extern "C" void teccl_pdlp_default_opts(teccl_pdlp_opts* o) {
   o->eps_infeas = 1e-6;
   o->infeas_every = 4;
   o->omega_bias = 1.0;
+  o->step_safety = 0.998;
   o->persist = 0;  // measured slower than the two-kernel iteration (profiles/r02_d_persist.md)
 }
 

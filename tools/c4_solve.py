@@ -53,6 +53,8 @@ line = {"workload": f"ALLGATHER {chassis}-chassis NDv2, 1 chunk, {mode}-link epo
         "device_seconds_max": float(secs), "ms_per_iteration": 1e3 * float(secs) / max(1, out["iters"]),
         "wall_s": wall, "cols": out["info"]["total_cols"], "rows": out["info"]["total_rows"],
         "per_rank_epochs": [out["info"]["k0"], out["info"]["k1"]], "pdlp": pdlp}
+if rank == 0:  # the solve's line first: certification below can take minutes
+    print(json.dumps(line), flush=True)
 if gather and rank == 0:
     import numpy as np
     from paper_2305_13479_b200.lp import completion_of
