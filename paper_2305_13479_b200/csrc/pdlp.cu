@@ -2565,8 +2565,14 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
     if (all_reduce(st, X, part, kGrid, pstride, 1, slots, world, rank, scal)) return TECCL_ECUDA;
     scale_by_kernel<<<gr, kThreads, 0, st>>>(n, xt, scal);
     nl += 1;
-    const int rounds = 40;
-    for (int it = 0; it < rounds; ++it) {
+    // 40 rounds, then blocks of 20 until the estimate moves by < 1e-6
+    // relative (at most 500 rounds): an estimate short of the norm makes the
+    // step too long, and on large LPs with clustered top singular values 40
+    // rounds are not enough (the 32-chassis LP diverged; DESIGN.md configs[4]).
+    // The decision uses the all-reduced value: identical on every rank.
+    const int min_rounds = 40, max_rounds = 500, block = 20;
+    double nv = 0.0, prev = -1.0;
+    for (int it = 0;; ++it) {
       mul_kernel<<<gr, kThreads, 0, st>>>(n, xbar, xt, rootD);
       X.halo(st, {A_XBAR});
       spmv_scaled_kernel<UNIT><<<gr, kThreads, 0, st>>>(m, lp->row_ptr, lp->col, lp->val, xbar_w, nullptr, yt);
@@ -2577,14 +2583,21 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
       sumsq_kernel<<<kGrid, kThreads, 0, st>>>(n, xt, part);
       nl += 6;
       if (all_reduce(st, X, part, kGrid, pstride, 1, slots, world, rank, scal)) return TECCL_ECUDA;
-      if (it + 1 < rounds) {
-        scale_by_kernel<<<gr, kThreads, 0, st>>>(n, xt, scal);
-        nl += 1;
+      const int done_rounds = it + 1;
+      if (done_rounds >= min_rounds && ((done_rounds - min_rounds) % block == 0 || done_rounds >= max_rounds)) {
+        TECCL_CUDA(cudaMemcpyAsync(&nv, scal, sizeof(double), cudaMemcpyDeviceToHost, st));
+        TECCL_CUDA(cudaStreamSynchronize(st));
+        // nv = ||M v||^2 with M = B^T B: sigma = nv^(1/4); 4e-6 on nv ~ 1e-6 on sigma
+        if (done_rounds >= max_rounds || !std::isfinite(nv) || (prev > 0.0 && fabs(nv - prev) <= 4e-6 * nv)) {
+          if (o->verbose > 0)
+            fprintf(stderr, "[teccl pdlp r%d] power iteration: %d rounds\n", rank, done_rounds);
+          break;
+        }
+        prev = nv;
       }
+      scale_by_kernel<<<gr, kThreads, 0, st>>>(n, xt, scal);
+      nl += 1;
     }
-    double nv = 0.0;
-    TECCL_CUDA(cudaMemcpyAsync(&nv, scal, sizeof(double), cudaMemcpyDeviceToHost, st));
-    TECCL_CUDA(cudaStreamSynchronize(st));
     if (nv > 0.0 && std::isfinite(nv)) sigma_max = sqrt(sqrt(nv));
     TECCL_CUDA(cudaMemsetAsync(xbar_w, 0, sizeof(double) * (ncw + 1), st));
     TECCL_CUDA(cudaMemsetAsync(y_w, 0, sizeof(double) * (nrw + 1), st));
