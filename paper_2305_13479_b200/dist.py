@@ -240,16 +240,20 @@ def solve_source_partitioned(t, d, cfg, opts=None, eps_rel: float = 1e-4, max_it
            "rel_dual_res": res.rel_dual_res, "device_seconds": res.solve_seconds,
            "kernel_launches": int(res.spmv_launches), "world": world, "rank": rank,
            "info": dict(info, total_cols=plan.num_vars, total_rows=plan.num_rows)}
-    if gather:
+    if gather:  # the full solution on rank 0 (gather="all": on every rank)
         own = (info["c0"], info["c1"], x[info["c0"]:info["c1"]].copy(),
                info["q0"], info["q1"], x[info["q0"]:info["q1"]].copy())
         pieces = [None] * world
-        dist.all_gather_object(pieces, own, group=group)
-        full = np.empty(plan.num_vars)
-        for c0, c1, xa, q0, q1, xb in pieces:
-            full[c0:c1] = xa
-            full[q0:q1] = xb
-        out["x"] = full
+        if gather == "all":
+            dist.all_gather_object(pieces, own, group=group)
+        else:
+            dist.gather_object(own, pieces if rank == 0 else None, dst=0, group=group)
+        if gather == "all" or rank == 0:
+            full = np.empty(plan.num_vars)
+            for c0, c1, xa, q0, q1, xb in pieces:
+                full[c0:c1] = xa
+                full[q0:q1] = xb
+            out["x"] = full
         out["plan"] = plan
     lp.close()
     return out

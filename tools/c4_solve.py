@@ -21,7 +21,7 @@ import torch.distributed as dist  # noqa: E402
 
 from paper_2305_13479_b200 import (EpochConfig, check_lp_schedule, epoch_duration,  # noqa: E402
                                    generate_demand)
-from paper_2305_13479_b200.dist import solve_partitioned  # noqa: E402
+from paper_2305_13479_b200.dist import solve_partitioned, solve_source_partitioned  # noqa: E402
 from paper_2305_13479_b200.topology import ndv2  # noqa: E402
 
 chassis = int(sys.argv[1]) if len(sys.argv) > 1 else 32
@@ -40,13 +40,15 @@ d = generate_demand("allgather", t, 1, 25000)
 cfg = EpochConfig(epoch_duration(t, 25000, mode, 1), K, mode, 1, 25000)
 pdlp = json.loads(os.environ.get("PDLP_OPTS", "{}"))
 t0 = time.perf_counter()
-out = solve_partitioned(t, d, cfg, eps_rel=eps, eps_res=eps_res, max_iters=max_iters, device=local,
-                        gather=bool(gather), pdlp=pdlp)
+scheme = os.environ.get("SCHEME", "epoch")  # "source": whole LP per rank, partitioned by source
+fn = solve_source_partitioned if scheme == "source" else solve_partitioned
+out = fn(t, d, cfg, eps_rel=eps, eps_res=eps_res, max_iters=max_iters, device=local,
+         gather=bool(gather), pdlp=pdlp)
 wall = time.perf_counter() - t0
 secs = torch.tensor([out["device_seconds"]], dtype=torch.float64, device=f"cuda:{local}")
 dist.all_reduce(secs, op=dist.ReduceOp.MAX)
 line = {"workload": f"ALLGATHER {chassis}-chassis NDv2, 1 chunk, {mode}-link epochs, K={K}, "
-                    f"epoch blocks over {world} GPUs",
+                    f"{'by source' if scheme == 'source' else 'epoch blocks'} over {world} GPUs",
         "n_gpus": world, "eps_rel": eps, "eps_res": eps_res,
         "criterion": "gap <= eps_rel, primal and dual residuals <= min(eps_rel, eps_res) (eps_res 0: eps_rel)",
         "status": out["status"], "iters": out["iters"], "restarts": out["restarts"],
@@ -54,7 +56,7 @@ line = {"workload": f"ALLGATHER {chassis}-chassis NDv2, 1 chunk, {mode}-link epo
         "rel_primal_res": out["rel_primal_res"], "rel_dual_res": out["rel_dual_res"],
         "device_seconds_max": float(secs), "ms_per_iteration": 1e3 * float(secs) / max(1, out["iters"]),
         "wall_s": wall, "cols": out["info"]["total_cols"], "rows": out["info"]["total_rows"],
-        "per_rank_epochs": [out["info"]["k0"], out["info"]["k1"]], "pdlp": pdlp}
+        "partition": {k: out["info"].get(k) for k in ("k0", "k1", "s0", "s1")}, "pdlp": pdlp}
 if rank == 0:  # the solve's line first: certification below can take minutes
     print(json.dumps(line), flush=True)
 if gather and rank == 0:
