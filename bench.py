@@ -137,7 +137,7 @@ def traffic_from_profile(kernel, lp_key):
 
 
 BIG_CHASSIS, BIG_K = 8, 1800
-BIG_ONE_GPU = (6233.757891518579, 42560)  # its 1e-4 solve on one B200 (objective, iterations)
+BIG_ONE_GPU = (6227.987959464124, 48448)  # its 1e-4 solve on one B200 (objective, iterations; profiles/r02_i_bench.log)
 
 
 def big_workload():
@@ -417,7 +417,7 @@ def run_b200(args, rank, world, local_rank):
                   "time_to_1e-4_s": ss["device_seconds"], "iters": ss["iters"],
                   "status": ss["status"], "objective": ss["objective"],
                   # multi-GPU parity: the same LP on one GPU (bench at N = 1,
-                  # profiles/r02_b_bench.log) stops after the same iterations
+                  # profiles/r02_i_bench.log) stops after the same iterations
                   "one_gpu_reference": {"objective": BIG_ONE_GPU[0], "iters": BIG_ONE_GPU[1]},
                   "objective_rel_diff_vs_one_gpu": abs(ss["objective"] - BIG_ONE_GPU[0]) / abs(BIG_ONE_GPU[0])}
     if rank != 0:
