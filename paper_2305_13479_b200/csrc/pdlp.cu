@@ -1157,6 +1157,9 @@ __global__ void __launch_bounds__(kThreads) col_seg_kernel(TeOp op, Vecs V, int 
 #ifndef TECCL_SEG_TMA
 #define TECCL_SEG_TMA 1
 #endif
+#ifndef TECCL_SEG_PF_NEXT
+#define TECCL_SEG_PF_NEXT 1
+#endif
 
 struct alignas(16) SegStage {  // 16-byte multiple: every warp's stage is a bulk-copy destination
   double y[kSegTask + 2];   // [first & ~1, round_up_even(first + cnt))
@@ -1188,6 +1191,14 @@ __global__ void __launch_bounds__(kThreads, TECCL_SEG_MINB) row_seg_kernel(TeOp 
 #pragma unroll
   for (int t = 0; t < kSegTPW; ++t)
     tks[t] = (w0 + t < op.n_rtask) ? __ldg(op.rtask + w0 + t) : make_int4(0, 0, 0, 0);
+#if TECCL_SEG_PF_NEXT
+  // the descriptor of the warp that takes this slot a wave later: into L2 now
+  // (at the block's start the descriptor load is an HBM miss, 10 % of the stalls)
+  {
+    constexpr int ahead = TECCL_SEG_PF_NEXT * kSMs * TECCL_SEG_MINB * (kThreads / 32);
+    if (lane == 0 && w0 + ahead < op.n_rtask) prefetch_l2(op.rtask + w0 + ahead);
+  }
+#endif
 #if TECCL_SEG_TMA
   static_assert(kSegTPW == 1, "TMA staging is per warp task");
   __shared__ __align__(16) SegStage stage[kThreads / 32];

@@ -679,6 +679,9 @@ __device__ __forceinline__ void seg_cols(const TeOp& o, const int4& t, int lane,
 #ifndef TECCL_CAP_U
 #define TECCL_CAP_U 4
 #endif
+#ifndef TECCL_CUM_SHFL
+#define TECCL_CUM_SHFL 1   // cumulative-read rows: previous Rc by warp shuffle
+#endif
 #ifndef TECCL_CONS_U
 #define TECCL_CONS_U 4     // interior conservation tasks: incident edges per round of gathers
 #endif
@@ -805,6 +808,26 @@ __device__ __forceinline__ void seg_rows(const TeOp& o, const int4& t, int lane,
     }
   } else if (kind == SEG_CUM) {                    // cum(p,k)
     const uint32_t rd0 = o.nF + (uint32_t)A * 2 * K;
+#if TECCL_CUM_SHFL
+    // Rc(p,k-1) is the previous lane's Rc: two loads per row instead of three,
+    // the same operands and operations (the task's first row loads its own)
+    double rdv[kSegPerLane], rcv[kSegPerLane];
+#pragma unroll
+    for (int h = 0; h < kSegPerLane; ++h) {
+      const int i = lane + 32 * h;
+      const uint32_t rd = rd0 + 2 * (uint32_t)(off + i);
+      rdv[h] = (i < cnt) ? __ldg(x + rd) : 0.0;
+      rcv[h] = (i < cnt) ? __ldg(x + rd + 1) : 0.0;
+    }
+    const double first_prev = (lane == 0 && off >= 1) ? __ldg(x + rd0 + 2 * (uint32_t)off - 1) : 0.0;
+#pragma unroll
+    for (int h = 0; h < kSegPerLane; ++h) {
+      double prev = __shfl_up_sync(0xffffffffu, rcv[h], 1);
+      const double carry = __shfl_sync(0xffffffffu, h > 0 ? rcv[h > 0 ? h - 1 : 0] : 0.0, 31);
+      if (lane == 0) prev = (h == 0) ? first_prev : carry;
+      if (lane + 32 * h < cnt) a[h] = rcv[h] - rdv[h] - prev;
+    }
+#else
 #pragma unroll
     for (int h = 0; h < kSegPerLane; ++h) {
       const int i = lane + 32 * h;
@@ -814,6 +837,7 @@ __device__ __forceinline__ void seg_rows(const TeOp& o, const int4& t, int lane,
         a[h] = __ldg(x + rd + 1) - __ldg(x + rd) - v_prev;
       }
     }
+#endif
   } else if (kind == SEG_BCAP) {                   // bcap(g,k): sum_s B(s,g,k)
     const uint32_t q0 = o.EK + (uint32_t)Bv * (K + 1) + off;
 #if TECCL_CAP_JOINT
