@@ -138,3 +138,42 @@ def test_certificate_off_for_feasible_lp_family():
         assert sol.status == "optimal", (K, sol.meta)
         assert np.isfinite(sol.objective)
         lp.close()
+
+
+def _golden_model(name, with_meta=True):
+    """A collsched Model as the hook receives it: the reference's own rows,
+    bounds and objective (the golden .npz is collsched's build_lp_model
+    output) and, like every Model build_lp_model makes, meta kind "lp" with
+    the inputs it was built from (lp.py:40-45)."""
+    meta_g, a = load_golden(name)
+    t, d, tau, K, blim = build(name)
+    rp, col, val = a["row_ptr"], a["col"], a["val"]
+    rows = [(list(zip(col[rp[r]:rp[r + 1]].tolist(), val[rp[r]:rp[r + 1]].tolist())),
+             a["row_lo"][r], a["row_hi"][r]) for r in range(len(rp) - 1)]
+    meta = {"kind": "lp", "topology": t, "demand": d,
+            "cfg": EpochConfig(tau, K, "fastest", 1, d.chunk_size),
+            "opts": ModelOptions(buffer_limit=blim)} if with_meta else {}
+    return meta_g, types.SimpleNamespace(
+        name="lp-alltoall", num_vars=len(a["var_lb"]), kinds=["C"] * len(a["var_lb"]),
+        lb=list(a["var_lb"]), ub=list(a["var_ub"]), rows=rows,
+        objective={j: -c for j, c in enumerate(a["obj"]) if c}, meta=meta)
+
+
+@pytest.mark.parametrize("name", ["dgx1_ag1_K8", "dgx1_ag1_K6", "ndv2x2_ag1_K24", "funnel_blimit_K4"])
+def test_hook_on_reference_model_data(name):
+    # through the hook with the reference's own model data: the status and
+    # objective the reference's HiGHS reported (golden.json)
+    meta_g, m = _golden_model(name)
+    sol = reference_solve(m, types.SimpleNamespace(time_limit=60.0, verbosity=0))
+    assert sol.status == meta_g["status"]
+    if sol.feasible:
+        assert sol.objective == pytest.approx(meta_g["objective"], rel=1e-4)
+        assert len(sol.x) == m.num_vars
+
+
+def test_hook_generic_upload_without_meta():
+    # a Model without build_lp_model's meta goes through the CSR upload
+    meta_g, m = _golden_model("dgx1_ag1_K8", with_meta=False)
+    sol = reference_solve(m, types.SimpleNamespace(time_limit=60.0, verbosity=0))
+    assert sol.status == "optimal"
+    assert sol.objective == pytest.approx(meta_g["objective"], rel=1e-4)
