@@ -2576,12 +2576,19 @@ int solve_impl(teccl_ctx* ctx, teccl_lp* lp, const teccl_pdlp_opts* o, double* x
     if (all_reduce(st, X, part, kGrid, pstride, 1, slots, world, rank, scal)) return TECCL_ECUDA;
     scale_by_kernel<<<gr, kThreads, 0, st>>>(n, xt, scal);
     nl += 1;
-    // 40 rounds, then blocks of 20 until the estimate moves by < 2e-5
-    // relative (at most 300 rounds): an estimate short of the norm makes the
-    // step too long, and on large LPs with clustered top singular values 40
-    // rounds are not enough (the 32-chassis LP diverged; DESIGN.md configs[4]).
-    // The decision uses the all-reduced value: identical on every rank.
-    const int min_rounds = 40, max_rounds = 300, block = 20;
+    // 40 rounds; on HBM-resident LPs (>= kAutoMatrixFreeCols columns in
+    // total) then blocks of 20 until the estimate moves by < 2e-5 relative
+    // (at most 300 rounds): an estimate short of the norm makes the step too
+    // long, and there 40 rounds are not enough (the 32-chassis LP's estimate
+    // was 4 % low and the solve diverged; DESIGN.md configs[4]), while the
+    // extra rounds cost a negligible part of the solve. On L2-resident LPs
+    // the rounds are launch-bound (~9 launches each) and would cost as much
+    // as the whole solve of a small LP; 40 rounds have been stable on every
+    // one of them. The decision uses the all-reduced value: identical on
+    // every rank.
+    const int64_t total_cols = lp->part_world > 1 ? lp->em_ncols : (int64_t)n;
+    const int min_rounds = 40, block = 20;
+    const int max_rounds = total_cols >= kAutoMatrixFreeCols ? 300 : min_rounds;
     double nv = 0.0, prev = -1.0;
     for (int it = 0;; ++it) {
       mul_kernel<<<gr, kThreads, 0, st>>>(n, xbar, xt, rootD);
