@@ -116,7 +116,10 @@ def simulate(sched, t, d, opts: SimOptions | None = None, threads: int = 0) -> S
     ent_s = np.array([nidx[s] for s, _, _ in entries], dtype=np.int32)
     ent_c = np.array([c for _, c, _ in entries], dtype=np.int32)
     ent_d = np.array([nidx[x] for _, _, x in entries], dtype=np.int32)
-    ev_s = np.fromiter((nidx[ev.source] for ev in events), dtype=np.int32, count=n)
+    try:
+        ev_s = np.fromiter((nidx[ev.source] for ev in events), dtype=np.int32, count=n)
+    except KeyError as exc:  # (the reference would report every such send as causality)
+        raise ScheduleError(f"event names source {exc.args[0]!r}, which is not a node") from None
     ev_c = np.fromiter((ev.chunk for ev in events), dtype=np.int32, count=n)
     e32 = edge.astype(np.int32)
     ev_src = np.array([nidx[e.src] for e in edges], dtype=np.int32)[e32] if n else np.zeros(0, np.int32)

@@ -60,6 +60,8 @@ def test_replay_input_errors_match_reference_messages():
         simulate(Schedule(tau, (ScheduleEvent(*e0),), -1, d.chunk_size), t, d)
     with pytest.raises(ValidationError):
         simulate(Schedule(tau, (), -1, d.chunk_size), t, d, SimOptions(switch_mode="hyper-edge"))
+    with pytest.raises(ScheduleError, match="not a node"):
+        simulate(Schedule(tau, (ScheduleEvent("nope", 0, 0, 1, 0, 1.0),), -1, d.chunk_size), t, d)
 
 
 def test_empty_schedule_reports_every_entry_unmet():
