@@ -57,7 +57,7 @@ line = {"workload": f"ALLGATHER {chassis}-chassis NDv2, 1 chunk, {mode}-link epo
         "device_seconds_max": float(secs), "ms_per_iteration": 1e3 * float(secs) / max(1, out["iters"]),
         "wall_s": wall, "cols": out["info"]["total_cols"], "rows": out["info"]["total_rows"],
         "partition": {k: out["info"].get(k) for k in ("k0", "k1", "s0", "s1")}, "pdlp": pdlp}
-if rank == 0:  # the solve's line first: certification below can take minutes
+if rank == 0 and gather:  # the solve's line first: certification below can take minutes
     print(json.dumps(line), flush=True)
 if gather and rank == 0:
     import numpy as np
