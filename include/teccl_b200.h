@@ -35,7 +35,7 @@ extern "C" {
 #define TECCL_ENODEV 4    /* no usable sm_100 device */
 
 /* solve status (teccl_pdlp_result.status) */
-#define TECCL_OPTIMAL 0        /* all three relative criteria <= eps */
+#define TECCL_OPTIMAL 0        /* gap <= eps_rel, residuals <= min(eps_rel, eps_res) */
 #define TECCL_ITER_LIMIT 1     /* max_iters reached */
 #define TECCL_TIME_LIMIT 2     /* time_limit reached */
 #define TECCL_PRIMAL_INFEASIBLE 3  /* Farkas certificate found (see eps_infeas) */
@@ -142,7 +142,7 @@ int teccl_lp_destroy(teccl_lp* lp);
  * LPs. Termination: relative duality gap <= eps_rel and relative primal and
  * dual residuals <= min(eps_rel, eps_res) (definitions in DESIGN.md); primal
  * infeasibility is certified on the device (eps_infeas) and reported as
- * TECCL_PRIMAL_INFEASIBLE, the reference's "infeasible" (solver.py:133-135).
+ * TECCL_PRIMAL_INFEASIBLE, the reference's "infeasible" (solver.py:133-134).
  */
 typedef struct {
   double eps_rel;          /* e.g. 1e-4 */
@@ -207,7 +207,7 @@ typedef struct {
   double rel_dual_res;
   double solve_seconds;    /* device time, scaling + iterations + unscaling */
   double omega;            /* final primal weight */
-  double step;             /* eta = 0.998 / ||A_scaled||_2 */
+  double step;             /* eta = step_safety / ||E^1/2 A D^1/2||_2 estimate */
   int64_t spmv_launches;   /* all kernel launches issued by the solve (setup + chunks) */
   double infeas_cert;      /* last Farkas certificate value / magnitude (> eps_infeas:
                               TECCL_PRIMAL_INFEASIBLE); 0 before the first evaluation */
