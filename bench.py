@@ -25,6 +25,9 @@ scaling, no data-path collective): `value` is the per-LP time, max over
 ranks (not divided by N); `throughput_lps_per_s` = N / value.
 `one_lp_across_gpus` (informational, strong scaling): the 8-chassis LP solved
 once across all N GPUs, partitioned by source (N = 1: one GPU).
+`flagship_lp_across_gpus` (N >= 4): configs[4], the 32-chassis LP (0.96e9
+columns), solved to the parity bar across the N GPUs by source (~11 min at
+N = 4; --no-flagship skips it).
 `reference_uncensored` (N = 1): the configs[0] family (1-chassis NDv2
 AllGather) at horizons where the reference's HiGHS finishes, both arms on
 the same LP in the same run.
@@ -138,6 +141,18 @@ def traffic_from_profile(kernel, lp_key):
 
 BIG_CHASSIS, BIG_K = 8, 1800
 BIG_ONE_GPU = (6227.987959464124, 48448)  # its 1e-4 solve on one B200 (objective, iterations; profiles/r02_i_bench.log)
+
+
+def flagship_workload():
+    """configs[4]: ALLGATHER on 32-chassis NDv2, 1 chunk, slowest-link epochs,
+    K = 2024 (2 % above K* = 64 * 31 + 3)."""
+    from paper_2305_13479_b200 import EpochConfig, epoch_duration, generate_demand
+    from paper_2305_13479_b200.topology import ndv2
+    ch = int(os.environ.get("BENCH_FLAGSHIP_CHASSIS", "32"))  # smaller: a quick check of this path
+    K = 2024 if ch == 32 else int(round((64 * (ch - 1) + 3) * 1.02))
+    t = ndv2(ch)
+    d = generate_demand("allgather", t, 1, 25000)
+    return t, d, EpochConfig(epoch_duration(t, 25000, "slowest", 1), K, "slowest", 1, 25000)
 
 
 def big_workload():
@@ -420,6 +435,35 @@ def run_b200(args, rank, world, local_rank):
                   # profiles/r02_i_bench.log) stops after the same iterations
                   "one_gpu_reference": {"objective": BIG_ONE_GPU[0], "iters": BIG_ONE_GPU[1]},
                   "objective_rel_diff_vs_one_gpu": abs(ss["objective"] - BIG_ONE_GPU[0]) / abs(BIG_ONE_GPU[0])}
+    # --- configs[4] (north_star's flagship: the 32-chassis LP, 0.96e9 columns,
+    # slowest-link epochs) across the job's GPUs at N >= 4, by source, to the
+    # parity bar (~11 min on 4 B200s; 1 / 2 GPUs:
+    # profiles/r02_g_config4_*), device time max over ranks
+    flagship = None
+    if world >= 4 and not args.no_flagship:
+        from paper_2305_13479_b200.dist import solve_source_partitioned
+        ft, fd, fc = flagship_workload()
+        out, err = None, None
+        try:
+            out = solve_source_partitioned(ft, fd, fc, eps_rel=EPS, eps_res=EPS_RES, device=dev,
+                                           max_iters=1_000_000,
+                                           pdlp={"step_safety": 0.9, "time_limit": 3000.0})
+        except Exception as exc:  # reported, not fatal: the headline above stands
+            err = f"{type(exc).__name__}: {exc}"[:300]
+        tt = torch.tensor([out["device_seconds"] if out else -1.0], dtype=torch.float64, device=f"cuda:{dev}")
+        tdist.all_reduce(tt, op=tdist.ReduceOp.MAX)
+        if out is None:
+            flagship = {"error": err}
+        else:
+            flagship = {"lp": f"configs[4]: ALLGATHER {len(ft.gpus) // 8}-chassis NDv2, 1 chunk, slowest-link "
+                              f"epochs, K={fc.K}: {out['info']['total_cols']} columns, "
+                              f"{out['info']['total_rows']} rows, parity bar",
+                        "partition": "by source", "n_gpus": world, "device_seconds": float(tt[0]),
+                        "iters": out["iters"], "status": out["status"], "objective": out["objective"],
+                        "rel_gap": out["rel_gap"], "rel_primal_res": out["rel_primal_res"],
+                        "rel_dual_res": out["rel_dual_res"],
+                        "one_gpu_reference": {"device_seconds": 2086.3, "iters": 183744,
+                                              "objective": 76140.70045778598}}
     if rank != 0:
         return
     cpu = uncensored = None
@@ -456,6 +500,7 @@ def run_b200(args, rank, world, local_rank):
         "gpu_launches": int(launches),
         "parity": parity,
         "one_lp_across_gpus": strong,
+        "flagship_lp_across_gpus": flagship,
         "solve": {"status": last.status, "iters": last.meta["iters"],
                   "restarts": last.meta["restarts"], "objective": last.objective,
                   "rel_gap": last.meta["rel_gap"], "rel_primal_res": last.meta["rel_primal_res"],
@@ -474,6 +519,8 @@ def main():
     ap.add_argument("--no-hbm-roofline", action="store_true")
     ap.add_argument("--no-strong", action="store_true",
                     help="skip the one-LP-across-all-GPUs (strong scaling) solve")
+    ap.add_argument("--no-flagship", action="store_true",
+                    help="skip the configs[4] solve across the GPUs (N >= 4)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
